@@ -1,0 +1,312 @@
+#!/usr/bin/env python
+"""Benchmark: batched AGFT tuner replay, tuner-steps/s on N B200s (BASELINE.json metric).
+
+Workload (one "step" = one pass of the whole hot path, SURVEY §8 rows a0–a11):
+BASELINE configs[3] = C4 — 65,536 tuners per GPU (16 α0 × 16 pruning settings × 256
+traces, diurnal + burst load), the full 107-arm grid, d = 7, 24 h = 108,000 decision
+windows.  Per step: reset tuners → [trace records (K1) → replay (K2)] × 24 chunks →
+stats (→ NCCL all-gather of stats when N > 1).  Weak scaling: every rank runs its own
+C4 shard (traces offset by rank), so total work grows with N.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...
+
+``--impl reference`` times the CPU oracle (the paper has no code; oracle/ is this
+tier's reference arm) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "tuner-steps/sec (device-timed) at 1/2/4/8 B200; % of HBM/FP64 roofline"
+UNIT = "tuner-steps/s"
+CHUNK = 4500                     # decision windows per replay launch (1 h of trace)
+FP64_UNITS_PER_SM = 64           # FP64 FMA lanes per SM (B200)
+N_SM = 148
+
+
+def flops_per_step(d: int, k_act_sum: float, steps: float) -> float:
+    """Algorithmic FP64 flops: per active arm d²+3d+3 (Eq. 1 score) + 5
+    (pruning bookkeeping); per step 3d²+8d+4 (Sherman–Morrison + RLS update) + 50
+    (response, reward, Welford, stats)."""
+    return k_act_sum * (d * d + 3 * d + 3 + 5) + steps * (3 * d * d + 8 * d + 4 + 50)
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def stop(self) -> dict:
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[1]))
+                mx = max(mx, float(r[2]))
+                for n, v in zip(names, r[5:9]):
+                    if v.strip().lower() == "active":
+                        reasons.add(n)
+            except (ValueError, IndexError):
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks() -> dict:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f)
+    return {}
+
+
+def run_cpu_baseline(cfg: dict, n_tuners: int, T: int) -> dict:
+    """The oracle as it stands on this host's cores, on a bounded sample of the workload."""
+    import oracle
+    from agft_inputs import tuner_params
+    params = tuner_params(cfg, list(range(n_tuners)))
+    cores = os.cpu_count() or 1
+    t = time.perf_counter()
+    oracle.run_batch(cfg, params, T, threads=cores)
+    dt = time.perf_counter() - t
+    return {"value": n_tuners * T / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"C4 tuners 0..{n_tuners - 1} (trace 0, all 256 hyper-parameter points) × {T} steps, "
+                      f"free-running, {dt:.1f} s on {cores} threads"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--T", type=int, default=None, help="override decision windows (debug only)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    from agft_inputs import named_config, tuner_params
+    cfg = named_config(args.config)
+    if args.T:
+        cfg["T"] = args.T
+    T = cfg["T"]
+
+    if args.impl == "reference":
+        return reference_arm(args, cfg, rank, world)
+
+    import numpy as np
+    import torch
+    import paper_2508_01744_b200 as pkg
+    from paper_2508_01744_b200 import TunerBatch, STATS_DTYPE
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    n = cfg["n_tuners"]
+    R = cfg["n_traces"]
+    params = tuner_params(cfg)                        # local trace ids 0..R-1
+    tb = TunerBatch(cfg, params, device=f"cuda:{local}", trace_base=rank * R)
+    stream = torch.cuda.current_stream()
+    chunk = min(CHUNK, T)
+    records = tb.new_records(chunk)
+    stats_out = tb.stats_tensor()
+    gathered = (torch.empty(world * stats_out.numel(), dtype=torch.uint8, device=stats_out.device)
+                if world > 1 else None)
+    n_chunks = (T + chunk - 1) // chunk
+    ev_replay = []
+
+    def one_step(timed: bool):
+        tb.reset()
+        t = 0
+        while t < T:
+            m = min(chunk, T - t)
+            tb.generate(t, m, records)
+            if timed:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                tb.replay(records, t, m)
+                e1.record(stream)
+                ev_replay.append((e0, e1))
+            else:
+                tb.replay(records, t, m)
+            t += m
+        pkg.agft_stats(tb.h, stats_out)
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, stats_out)
+
+    for _ in range(args.warmup):
+        one_step(False)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    start.record(stream)
+    for _ in range(args.steps):
+        one_step(True)
+    end.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = start.elapsed_time(end)
+    replay_ms = sum(a.elapsed_time(b) for a, b in ev_replay)
+    if world > 1:
+        t_ = torch.tensor([ms], dtype=torch.float64, device=stats_out.device)
+        dist.all_reduce(t_, op=dist.ReduceOp.MAX)
+        ms = float(t_.item())
+
+    st = stats_out.cpu().numpy().view(STATS_DTYPE)
+    steps_ok = bool(np.all(st["steps"] == T)) and bool(np.all(st["flags"] == 0))
+    units = float(n) * T * world * args.steps
+    value = units / (ms / 1e3)
+
+    # roofline of the dominant kernel (replay): algorithmic FP64 flops / its event time
+    sum_active = float(np.sum(st["sum_active"], dtype=np.float64))
+    flops_rank_step = flops_per_step(cfg["d"], sum_active, float(n) * T)
+    achieved = flops_rank_step * args.steps / (replay_ms / 1e3) / 1e12
+    pk = peaks()
+    sm_mhz = float(pk.get("sm_max_mhz", 1965.0))
+    peak_fp64 = N_SM * FP64_UNITS_PER_SM * 2 * sm_mhz * 1e6 / 1e12
+    roofline = {"bound": "alu", "achieved": round(achieved, 4), "peak": round(peak_fp64, 2),
+                "unit": "TFLOP/s", "frac": round(achieved / peak_fp64, 5), "traffic": None,
+                "kernel": "replay_kernel", "replay_share": round(replay_ms / ms, 4),
+                "peak_source": "derived: 148 SM × 64 FP64 FMA/clk × 2 × sm_max_mhz (DESIGN.md §5)",
+                "mean_active_arms": round(sum_active / (float(n) * T), 3)}
+
+    out = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": f"{args.config}: {n} tuners/GPU × {cfg['n_arms']} arms × d={cfg['d']} × "
+                                  f"{T} windows ({R} traces/GPU, α×pruning sweep, diurnal+burst)",
+                      "tuners_per_gpu": n, "T": T, "arms": cfg["n_arms"], "d": cfg["d"],
+                      "traces_per_gpu": R, "chunk": chunk,
+                      "l2": f"inputs larger than L2: tuner state {tb.workspace.numel() / 2**30:.2f} GiB/GPU",
+                      "parallelism": f"tuner shards dp{world}"},
+           "roofline": roofline, "clocks": clk,
+           "gpu_launches": args.steps * (2 + 2 * n_chunks), "all_steps_complete": steps_ok}
+
+    if not args.no_e2e:
+        out["e2e"] = e2e_leg(cfg, params, rank, world, local, chunk, n, T, args)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = run_cpu_baseline(cfg, 256, T)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def e2e_leg(cfg, params, rank, world, local, chunk, n, T, args) -> dict:
+    """Same metric through agft_run with HOST params/stats: H2D of the per-tuner params and
+    D2H of the per-tuner stats are inside the timed region, every step."""
+    import numpy as np
+    import torch
+    import paper_2508_01744_b200 as pkg
+    from paper_2508_01744_b200 import make_config, make_params, STATS_DTYPE
+    dev = torch.device("cuda", local)
+    cfg_c = make_config(cfg, n_tuners=n, n_traces=cfg["n_traces"], trace_base=rank * cfg["n_traces"])
+    ws = torch.empty(pkg.agft_workspace_bytes(cfg_c), dtype=torch.uint8, device=dev)
+    scratch = torch.empty(cfg["n_traces"] * chunk * pkg.RECORD_BYTES, dtype=torch.uint8, device=dev)
+    hp = torch.from_numpy(make_params(params).view(np.uint8)).pin_memory()
+    dp = torch.empty_like(hp, device=dev)
+    ds = torch.empty(n * STATS_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+    hs = torch.empty(n * STATS_DTYPE.itemsize, dtype=torch.uint8).pin_memory()
+    pkg.agft_run(cfg_c, hp, dp, T, chunk, ws, scratch, ds, hs)          # warm-up
+    reps = max(1, min(args.steps, 2))
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    t = time.perf_counter()
+    for _ in range(reps):
+        pkg.agft_run(cfg_c, hp, dp, T, chunk, ws, scratch, ds, hs)
+    dt = time.perf_counter() - t
+    if world > 1:
+        import torch.distributed as dist
+        t_ = torch.tensor([dt], dtype=torch.float64, device=dev)
+        dist.all_reduce(t_, op=dist.ReduceOp.MAX)
+        dt = float(t_.item())
+    return {"value": round(n * T * world * reps / dt, 1), "unit": UNIT, "h2d_bytes_per_step": hp.numel(),
+            "d2h_bytes_per_step": hs.numel(), "api": "agft_run (host params in, host stats out)",
+            "steps": reps}
+
+
+def reference_arm(args, cfg, rank, world):
+    """The oracle (this tier's reference arm) on the box's host cores, rank 0 only."""
+    if rank != 0:
+        return
+    import oracle
+    from agft_inputs import tuner_params
+    T = cfg["T"]
+    n_sample = 64
+    params = tuner_params(cfg, list(range(n_sample)))
+    cores = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        oracle.run_batch(cfg, params, min(T, 2000), threads=cores)
+    t = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.run_batch(cfg, params, T, threads=cores)
+    dt = time.perf_counter() - t
+    value = n_sample * T * args.steps / dt
+    sample = f"C4 tuners 0..{n_sample - 1} × {T} windows per step, free-running"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3 / args.steps, 1),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": f"{args.config} (bounded sample)", "sample": sample},
+        "cpu_baseline": {"value": round(value, 1), "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": round(value, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
+        flush=True)
+
+
+if __name__ == "__main__":
+    main()

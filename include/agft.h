@@ -1,0 +1,191 @@
+/*
+ * agft.h — C ABI of the B200-native AGFT hot path (ABI version 1).
+ *
+ * What it computes: a batched replay of N independent AGFT frequency tuners
+ * (arXiv 2508.01744 §4), each a contextual LinUCB bandit over a frequency grid,
+ * against a synthetic serving trace and a closed-form latency/power response
+ * (ENV.md).  One call advances every tuner by one or many decision windows.
+ *
+ * Conventions (all entry points):
+ *  - Pointers prefixed d_ are DEVICE pointers, h_ are HOST pointers.  Every device
+ *    buffer is allocated and owned by the caller (PyTorch); the library never
+ *    allocates device memory.  The opaque handle is host memory owned by the library.
+ *  - Calls are asynchronous and ordered on the stream given to agft_create (a
+ *    cudaStream_t passed as void*).  Only agft_create and agft_run synchronise.
+ *  - Errors are returned as negative agft_status codes; nothing is thrown.  A CUDA
+ *    error is sticky on the handle (every later call returns AGFT_E_CUDA).
+ *  - A handle is not thread-safe (single writer).
+ *  - Device-side anomalies never abort: a non-finite EDP or reward sets bit 0 of
+ *    the tuner's stats.flags and freezes that tuner.
+ *  - Layout and arithmetic of every step follow ENV.md (the contract shared with
+ *    the CPU oracle, which is a separate implementation).
+ */
+#ifndef AGFT_H
+#define AGFT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AGFT_ABI_VERSION 1u
+#define AGFT_MAX_ARMS 128u          /* K ≤ 128 */
+#define AGFT_MAX_D 7u               /* the paper's 7-dim context */
+#define AGFT_MAX_WINDOW 64u         /* reward-median window, AMB-3 */
+#define AGFT_RECORD_BYTES 128u      /* ENV.md §3.2 per-window step record */
+#define AGFT_ROW_WORDS 12u          /* ENV.md §2.2 raw trace row (uint32) */
+#define AGFT_NO_RECORD 0xFFFFFFFFu  /* agft_tuner_params.record_slot: not recorded */
+
+typedef struct agft_handle_s *agft_handle;
+
+typedef enum {
+    AGFT_OK = 0,
+    AGFT_E_INVALID_ARG = -1,  /* NULL pointer, zero size, bad enum */
+    AGFT_E_INVALID_GRID = -2, /* step = 0, K ∉ [1,128], f_min+(K-1)·step > f_max_hw */
+    AGFT_E_EMPTY_ARMS = -3,   /* an empty arm set */
+    AGFT_E_DIM = -4,          /* d ∉ [1,7] */
+    AGFT_E_NONFINITE = -5,    /* a non-finite or out-of-range coefficient */
+    AGFT_E_WORKSPACE = -6,    /* workspace too small or misaligned */
+    AGFT_E_STATE = -7,        /* t0 disagrees with the handle's step counter */
+    AGFT_E_CUDA = -8,         /* a CUDA launch/runtime error (sticky) */
+    AGFT_E_DEVICE = -9        /* no sm_100 device / wrong architecture */
+} agft_status;
+
+/* Frequency grid: arm k ↔ f_min + k·step MHz; f_max_hw bounds the grid and
+ * sets the cascade threshold. */
+typedef struct { uint32_t f_min_mhz, f_step_mhz, n_arms, f_max_hw_mhz; } agft_grid;
+
+/* Pruning, P:387-391 / S:255-258. The per-tuner thresholds (extreme reward
+ * threshold, historical k) live in agft_tuner_params (sweep axes). */
+typedef struct {
+    uint32_t enable, extreme_round_limit, extreme_min_samples, historical_min_round,
+             historical_min_samples, pad;
+    double cascade_fraction;
+} agft_prune;
+
+/* Policy: α_t = α0/√(1+t/τ) (AMB-1), reward = clip(1 − EDP/median, lo, hi) over the
+ * last median_window EDPs (AMB-3), near-tie tolerance (ENV.md §4.5). */
+typedef struct { double tau, clip_lo, clip_hi, tie_rel; uint32_t median_window, pad; } agft_policy;
+
+/* ENV-R constants (ENV.md §3). */
+typedef struct {
+    double window_s, p_idle, k_lin, k_cube, u_floor, u_max, c_prefill, c_decode, beta,
+           sigma_e, sigma_t;
+} agft_env;
+
+/* ENV-T constants (ENV.md §2.1). */
+typedef struct {
+    double lambda0, burst_mult, t_iter0, t_iter1, e2e0, tau_ref;
+    uint32_t seg_steps, steps_per_hour, burst_steps, burst_p32, cap, kv_total, pattern_mode, pad;
+    uint32_t ctx_lo[5], ctx_hi[5], gen_lo[5], gen_hi[5], weight[5], pad2;
+    double conc_mult[5], hit_rate[5], knot[24];
+} agft_trace_cfg;
+
+typedef struct {
+    uint32_t abi_version;     /* must be AGFT_ABI_VERSION */
+    uint32_t n_tuners;        /* N ≥ 1 */
+    uint32_t d;               /* context dims, first d of x1..x7 (AMB-17) */
+    uint32_t n_traces;        /* R: traces held by this handle (local ids 0..R-1) */
+    uint32_t trace_base;      /* global id of local trace 0 (Philox key, ENV.md §1) */
+    uint32_t record_slots;    /* rows of d_traj / d_gap in agft_replay (0 = none) */
+    agft_grid grid;
+    agft_prune prune;
+    agft_policy policy;
+    agft_env env;
+    agft_trace_cfg trace;
+    double norm_lo[7], norm_hi[7];   /* context normalisation bounds (AMB-14) */
+    uint64_t env_seed;               /* S in ENV.md §1 */
+} agft_config;
+
+/* Per-tuner parameters (the hyper-parameter sweep axes of C4/C5). */
+typedef struct {
+    uint32_t trace_id;        /* LOCAL trace index in [0, n_traces) */
+    uint32_t record_slot;     /* row of d_traj/d_gap, or AGFT_NO_RECORD */
+    double alpha0;            /* ≥ 0 (0 = greedy, Eq. 2) */
+    double extreme_reward_threshold; /* τ_E, P:387 (−1.2) */
+    double historical_k;      /* k_h, P:388 (1.0) */
+} agft_tuner_params;          /* 32 B */
+
+/* Per-tuner statistics (ENV.md §4.9), 104 B. */
+typedef struct {
+    uint64_t traj_hash;       /* FNV-1a over the chosen arm of every step */
+    uint64_t sum_active;      /* Σ_t |F_available(t)| before pruning (work counter) */
+    uint32_t steps, last_arm, n_active, n_pruned_extreme, n_pruned_hist, n_pruned_cascade,
+             near_tie_steps, flags;
+    double sum_energy, sum_tpot, sum_ttft, sum_edp, sum_reward, base_energy, base_edp;
+} agft_tuner_stats;
+
+/* Host-only validation of a config (the checks agft_create makes before touching
+ * the device): grid, dimensions, finiteness/ranges. */
+agft_status agft_validate(const agft_config *cfg);
+
+/* sizeof of the ABI structs as compiled: which = 0 agft_config, 1 agft_tuner_params,
+ * 2 agft_tuner_stats (lets bindings check their mirrors). */
+uint32_t agft_struct_size(int which);
+
+/* Bytes of device workspace a config needs (0 if the config is invalid). The
+ * workspace must be 256-byte aligned. */
+size_t agft_workspace_bytes(const agft_config *cfg);
+
+/* Validate cfg, lay out d_workspace, copy d_params [n_tuners] into it and initialise
+ * every tuner: A⁻¹ = I, θ = b = 0, all arms active, empty EDP window (AMB-2).
+ * stream is a cudaStream_t (NULL = legacy default stream).  Synchronises once. */
+agft_status agft_create(const agft_config *cfg, const agft_tuner_params *d_params,
+                        void *d_workspace, size_t ws_bytes, void *stream, agft_handle *out);
+
+/* Re-initialise every tuner of the handle (as agft_create does, keeping its params)
+ * and set the step counter to 0.  Asynchronous. */
+agft_status agft_reset(agft_handle h);
+
+/* ENV-T + the per-window record for steps [t0, t0+n_steps) of every local trace:
+ * d_records = [n_traces][n_steps][128 B] (ENV.md §3.2), d_raw = [n_traces][n_steps][12]
+ * uint32 raw rows (ENV.md §2.2) or NULL.  Independent of tuner state. */
+agft_status agft_trace_generate(agft_handle h, uint32_t t0, uint32_t n_steps, void *d_records,
+                                uint32_t *d_raw);
+
+/* One decision window for every tuner (Eq. 1 → response → reward → Eqs. 3–5 → §4.3)
+ * at the handle's current step t; d_records = [n_traces][1][128 B] for step t;
+ * d_chosen = [n_tuners] chosen arm index, or NULL.  Advances t by 1. */
+agft_status agft_step(agft_handle h, const void *d_records, uint32_t *d_chosen);
+
+/* n_steps decision windows for every tuner, steps [t0, t0+n_steps); t0 must equal the
+ * handle's step counter (AGFT_E_STATE otherwise).  d_records = [n_traces][n_steps][128 B].
+ * d_traj = [record_slots][n_steps] chosen arms and d_gap = [record_slots][n_steps]
+ * relative top-2 score gaps (ENV.md §4.5) for tuners with a record_slot; either may be NULL. */
+agft_status agft_replay(agft_handle h, const void *d_records, uint32_t t0, uint32_t n_steps,
+                        uint8_t *d_traj, double *d_gap);
+
+/* Copy the per-tuner statistics into d_out [n_tuners]. */
+agft_status agft_stats(agft_handle h, agft_tuner_stats *d_out);
+
+/* One tuner's arm state (for checkpoints and parity): d_ainv_packed [K][d(d+1)/2]
+ * (row-major upper triangle of A⁻¹), d_b [K][d], d_theta [K][d], d_n [K], d_rbar [K],
+ * d_ebar [K], d_active_mask [4] (bit k of word k/32).  Any pointer may be NULL. */
+agft_status agft_export_arms(agft_handle h, uint32_t tuner, double *d_ainv_packed, double *d_b,
+                             double *d_theta, uint32_t *d_n, double *d_rbar, double *d_ebar,
+                             uint32_t *d_active_mask);
+
+/* The handle's current step counter. */
+agft_status agft_get_step(agft_handle h, uint32_t *t);
+
+/* End to end from HOST buffers: copies h_params [n_tuners] host→device, creates the
+ * tuners in d_workspace, replays steps [0, n_steps) generating the trace in chunks of
+ * chunk_steps into d_scratch (≥ n_traces·chunk_steps·128 B), and copies the statistics
+ * device→host into h_stats [n_tuners].  d_params_buf is a device buffer of n_tuners
+ * agft_tuner_params and d_stats_buf of n_tuners agft_tuner_stats.  Synchronises. */
+agft_status agft_run(const agft_config *cfg, const agft_tuner_params *h_params,
+                     agft_tuner_params *d_params_buf, uint32_t n_steps, uint32_t chunk_steps,
+                     void *d_workspace, size_t ws_bytes, void *d_scratch, size_t scratch_bytes,
+                     agft_tuner_stats *d_stats_buf, agft_tuner_stats *h_stats, void *stream);
+
+/* Frees the host handle only; the caller frees its device buffers. */
+agft_status agft_destroy(agft_handle h);
+
+const char *agft_status_string(agft_status s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AGFT_H */

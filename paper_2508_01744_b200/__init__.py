@@ -1,0 +1,224 @@
+"""B200-native AGFT hot path: a batched replay of LinUCB GPU-frequency tuners.
+
+The Python layer marshals arguments into the C ABI of ``include/agft.h``
+(``libagft.so``, hand-written sm_100a kernels). PyTorch provides device memory,
+streams and process groups only. Names follow the ABI: ``agft_create``,
+``agft_trace_generate``, ``agft_step``, ``agft_replay``, ``agft_stats``,
+``agft_export_arms``, ``agft_run``, ``agft_destroy``. ``TunerBatch`` bundles them.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _abi
+from ._abi import (NO_RECORD, PARAMS_DTYPE, RECORD_BYTES, ROW_WORDS, STATS_DTYPE, AgftError,
+                   make_config, make_params)
+
+__all__ = ["agft_workspace_bytes", "agft_create", "agft_reset", "agft_trace_generate", "agft_step", "agft_replay",
+           "agft_stats", "agft_export_arms", "agft_get_step", "agft_run", "agft_destroy",
+           "TunerBatch", "make_config", "make_params", "PARAMS_DTYPE", "STATS_DTYPE", "NO_RECORD",
+           "RECORD_BYTES", "ROW_WORDS", "AgftError", "lib_path"]
+
+
+def lib_path() -> str:
+    return _abi.LIB_PATH
+
+
+def _p(t):
+    """Device (or host) pointer of a torch tensor / numpy array, or None."""
+    if t is None:
+        return None
+    if isinstance(t, np.ndarray):
+        return t.ctypes.data
+    return t.data_ptr()
+
+
+def _stream(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream
+
+
+def agft_workspace_bytes(cfg_c: _abi.AgftConfig) -> int:
+    return int(_abi.lib().agft_workspace_bytes(C.byref(cfg_c)))
+
+
+def agft_create(cfg_c, d_params, workspace, stream=None) -> int:
+    h = C.c_void_p()
+    _abi.check("agft_create", _abi.lib().agft_create(C.byref(cfg_c), _p(d_params), _p(workspace),
+                                                      workspace.numel() * workspace.element_size(),
+                                                      _stream(stream), C.byref(h)))
+    return h.value
+
+
+def agft_reset(h):
+    _abi.check("agft_reset", _abi.lib().agft_reset(h))
+
+
+def agft_trace_generate(h, t0, n_steps, records, raw=None):
+    _abi.check("agft_trace_generate", _abi.lib().agft_trace_generate(h, t0, n_steps, _p(records), _p(raw)))
+
+
+def agft_step(h, records, chosen=None):
+    _abi.check("agft_step", _abi.lib().agft_step(h, _p(records), _p(chosen)))
+
+
+def agft_replay(h, records, t0, n_steps, traj=None, gap=None):
+    _abi.check("agft_replay", _abi.lib().agft_replay(h, _p(records), t0, n_steps, _p(traj), _p(gap)))
+
+
+def agft_stats(h, out):
+    _abi.check("agft_stats", _abi.lib().agft_stats(h, _p(out)))
+
+
+def agft_export_arms(h, tuner, ainv=None, b=None, theta=None, n=None, rbar=None, ebar=None, mask=None):
+    _abi.check("agft_export_arms", _abi.lib().agft_export_arms(h, tuner, _p(ainv), _p(b), _p(theta),
+                                                                _p(n), _p(rbar), _p(ebar), _p(mask)))
+
+
+def agft_get_step(h) -> int:
+    t = C.c_uint32()
+    _abi.check("agft_get_step", _abi.lib().agft_get_step(h, C.byref(t)))
+    return t.value
+
+
+def agft_run(cfg_c, h_params, d_params_buf, n_steps, chunk_steps, workspace, scratch, d_stats_buf,
+             h_stats, stream=None):
+    _abi.check("agft_run", _abi.lib().agft_run(
+        C.byref(cfg_c), _p(h_params), _p(d_params_buf), n_steps, chunk_steps, _p(workspace),
+        workspace.numel() * workspace.element_size(), _p(scratch),
+        scratch.numel() * scratch.element_size(), _p(d_stats_buf), _p(h_stats), _stream(stream)))
+
+
+def agft_destroy(h):
+    _abi.check("agft_destroy", _abi.lib().agft_destroy(h))
+
+
+class TunerBatch:
+    """N tuners on one GPU: owns (torch-allocated) workspace, params and the handle."""
+
+    def __init__(self, cfg: dict, params: dict, device="cuda", record_slot=None, trace_base: int = 0,
+                 n_traces: int | None = None, stream=None):
+        import torch
+        self.cfg = cfg
+        self.device = torch.device(device)
+        self.n = len(params["trace_id"])
+        self.n_traces = cfg["n_traces"] if n_traces is None else n_traces
+        rec_slots = 0 if record_slot is None else int(np.max(np.where(
+            np.asarray(record_slot) == NO_RECORD, -1, record_slot)) + 1)
+        self.record_slots = rec_slots
+        self.cfg_c = make_config(cfg, n_tuners=self.n, n_traces=self.n_traces, trace_base=trace_base,
+                                 record_slots=rec_slots)
+        ws = agft_workspace_bytes(self.cfg_c)
+        if ws == 0:
+            raise AgftError("agft_workspace_bytes", -1)
+        self.workspace = torch.empty(ws, dtype=torch.uint8, device=self.device)
+        host = make_params(params, record_slot)
+        self.d_params = torch.from_numpy(host.view(np.uint8)).to(self.device)
+        self.stream = stream
+        self.h = agft_create(self.cfg_c, self.d_params, self.workspace, stream)
+
+    def reset(self):
+        agft_reset(self.h)
+
+    @property
+    def t(self) -> int:
+        return agft_get_step(self.h)
+
+    def new_records(self, n_steps: int):
+        import torch
+        return torch.empty((self.n_traces, n_steps, RECORD_BYTES), dtype=torch.uint8, device=self.device)
+
+    def generate(self, t0: int, n_steps: int, records=None, raw: bool = False):
+        import torch
+        records = self.new_records(n_steps) if records is None else records
+        rawt = (torch.empty((self.n_traces, n_steps, ROW_WORDS), dtype=torch.int32, device=self.device)
+                if raw else None)
+        agft_trace_generate(self.h, t0, n_steps, records, rawt)
+        return (records, rawt) if raw else records
+
+    def replay(self, records, t0: int, n_steps: int, record: bool = False):
+        import torch
+        traj = gap = None
+        if record and self.record_slots:
+            traj = torch.zeros((self.record_slots, n_steps), dtype=torch.uint8, device=self.device)
+            gap = torch.zeros((self.record_slots, n_steps), dtype=torch.float64, device=self.device)
+        agft_replay(self.h, records, t0, n_steps, traj, gap)
+        return traj, gap
+
+    def step(self, records_t):
+        import torch
+        chosen = torch.empty(self.n, dtype=torch.int32, device=self.device)
+        agft_step(self.h, records_t, chosen)
+        return chosen
+
+    def run(self, T: int, chunk: int = 4500, record: bool = False):
+        """Generate + replay steps [t, T) in chunks; returns recorded traj/gap (host) if asked."""
+        import torch
+        trajs, gaps = [], []
+        rec = None
+        t = self.t
+        while t < T:
+            n = min(chunk, T - t)
+            if rec is None or rec.shape[1] != n:
+                rec = self.new_records(n)
+            self.generate(t, n, rec)
+            tr, gp = self.replay(rec, t, n, record=record)
+            if record and tr is not None:
+                trajs.append(tr.cpu())
+                gaps.append(gp.cpu())
+            t += n
+        if record and trajs:
+            return torch.cat(trajs, 1).numpy(), torch.cat(gaps, 1).numpy()
+        return None, None
+
+    def stats_tensor(self):
+        import torch
+        out = torch.empty(self.n * STATS_DTYPE.itemsize, dtype=torch.uint8, device=self.device)
+        agft_stats(self.h, out)
+        return out
+
+    def stats(self) -> np.ndarray:
+        return self.stats_tensor().cpu().numpy().view(STATS_DTYPE)
+
+    def export_arms(self, tuner: int) -> dict:
+        import torch
+        K, d = self.cfg["n_arms"], self.cfg["d"]
+        P = d * (d + 1) // 2
+        dev = self.device
+        out = {"ainv_packed": torch.empty((K, P), dtype=torch.float64, device=dev),
+               "b": torch.empty((K, d), dtype=torch.float64, device=dev),
+               "theta": torch.empty((K, d), dtype=torch.float64, device=dev),
+               "n": torch.empty(K, dtype=torch.int32, device=dev),
+               "rbar": torch.empty(K, dtype=torch.float64, device=dev),
+               "ebar": torch.empty(K, dtype=torch.float64, device=dev),
+               "mask": torch.empty(4, dtype=torch.int32, device=dev)}
+        agft_export_arms(self.h, tuner, out["ainv_packed"], out["b"], out["theta"], out["n"],
+                         out["rbar"], out["ebar"], out["mask"])
+        res = {k: v.cpu().numpy() for k, v in out.items()}
+        res["n"] = res["n"].view(np.uint32)
+        m = res.pop("mask").view(np.uint32)
+        res["active"] = np.array([(m[k // 32] >> (k % 32)) & 1 for k in range(K)], dtype=np.uint8)
+        ainv = np.zeros((K, d, d))
+        e = 0
+        for i in range(d):
+            for j in range(i, d):
+                ainv[:, i, j] = res["ainv_packed"][:, e]
+                ainv[:, j, i] = res["ainv_packed"][:, e]
+                e += 1
+        res["Ainv"] = ainv
+        return res
+
+    def close(self):
+        if getattr(self, "h", None):
+            agft_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,314 @@
+// host.cu — the C-ABI entry points of include/agft.h: validation, workspace layout,
+// launches, status codes.  No device allocation happens here: every device buffer
+// is the caller's.
+#include <cmath>
+#include <cstring>
+#include <new>
+
+#include "agft_internal.cuh"
+
+using namespace agft;
+
+struct agft_handle_s {
+    agft_config cfg;
+    Layout layout;
+    Ws ws;
+    cudaStream_t stream;
+    uint32_t t;             // current global step (observe/apply alternate strictly)
+    agft_status sticky;     // AGFT_OK or AGFT_E_CUDA
+};
+
+namespace {
+
+bool finite(double v) { return std::isfinite(v); }
+
+agft_status validate(const agft_config *c)
+{
+    if (!c) return AGFT_E_INVALID_ARG;
+    if (c->abi_version != AGFT_ABI_VERSION) return AGFT_E_INVALID_ARG;
+    if (c->n_tuners == 0 || c->n_traces == 0) return AGFT_E_INVALID_ARG;
+    const agft_grid &g = c->grid;
+    if (g.n_arms == 0) return AGFT_E_EMPTY_ARMS;
+    if (g.f_step_mhz == 0 || g.n_arms > AGFT_MAX_ARMS || g.f_min_mhz == 0) return AGFT_E_INVALID_GRID;
+    if ((uint64_t)g.f_min_mhz + (uint64_t)(g.n_arms - 1) * g.f_step_mhz > g.f_max_hw_mhz) return AGFT_E_INVALID_GRID;
+    if (c->d < 1 || c->d > AGFT_MAX_D) return AGFT_E_DIM;
+    for (int i = 0; i < 7; ++i)
+        if (!finite(c->norm_lo[i]) || !finite(c->norm_hi[i]) || c->norm_lo[i] > c->norm_hi[i]) return AGFT_E_NONFINITE;
+    const agft_policy &p = c->policy;
+    if (!finite(p.tau) || p.tau <= 0 || !finite(p.clip_lo) || !finite(p.clip_hi) || p.clip_lo > p.clip_hi ||
+        !finite(p.tie_rel) || p.tie_rel < 0)
+        return AGFT_E_NONFINITE;
+    if (p.median_window < 1 || p.median_window > AGFT_MAX_WINDOW) return AGFT_E_INVALID_ARG;
+    const agft_env &e = c->env;
+    const double ev[] = {e.window_s, e.p_idle, e.k_lin, e.k_cube, e.u_floor, e.u_max, e.c_prefill,
+                         e.c_decode, e.beta, e.sigma_e, e.sigma_t};
+    for (double v : ev)
+        if (!finite(v) || v < 0) return AGFT_E_NONFINITE;
+    if (e.window_s <= 0 || e.u_max <= 0 || e.u_max >= 1 || e.sigma_e >= 1 || e.sigma_t >= 1 || e.c_decode <= 0 ||
+        e.beta > 1)
+        return AGFT_E_NONFINITE;
+    const agft_trace_cfg &t = c->trace;
+    if (t.seg_steps == 0 || t.steps_per_hour == 0 || t.burst_steps == 0 || t.cap == 0 || t.kv_total == 0 ||
+        t.pattern_mode > 4)
+        return AGFT_E_INVALID_ARG;
+    if (!finite(t.lambda0) || t.lambda0 < 0 || !finite(t.t_iter0) || t.t_iter0 <= 0 || !finite(t.t_iter1) ||
+        t.t_iter1 < 0 || !finite(t.e2e0) || !finite(t.tau_ref) || !finite(t.burst_mult))
+        return AGFT_E_NONFINITE;
+    uint32_t wsum = 0;
+    for (int i = 0; i < 5; ++i) {
+        wsum += t.weight[i];
+        if (t.ctx_hi[i] < t.ctx_lo[i] || t.gen_hi[i] < t.gen_lo[i]) return AGFT_E_INVALID_ARG;
+        if (!finite(t.conc_mult[i]) || t.conc_mult[i] < 0 || !finite(t.hit_rate[i]) || t.hit_rate[i] < 0 ||
+            t.hit_rate[i] > 1)
+            return AGFT_E_NONFINITE;
+    }
+    if (wsum != 256) return AGFT_E_INVALID_ARG;
+    for (int i = 0; i < 24; ++i)
+        if (!finite(t.knot[i]) || t.knot[i] < 0) return AGFT_E_NONFINITE;
+    if (!finite(c->prune.cascade_fraction) || c->prune.cascade_fraction <= 0 || c->prune.cascade_fraction > 1)
+        return AGFT_E_NONFINITE;
+    return AGFT_OK;
+}
+
+agft_status cuda_status(agft_handle h, cudaError_t e)
+{
+    if (e == cudaSuccess) return AGFT_OK;
+    if (h) h->sticky = AGFT_E_CUDA;
+    return AGFT_E_CUDA;
+}
+
+ReplayArgs replay_args(agft_handle h, const void *records, uint32_t t0, uint32_t n_steps)
+{
+    const agft_config &c = h->cfg;
+    ReplayArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.w = h->ws;
+    a.records = static_cast<const StepRec *>(records);
+    a.n_tuners = c.n_tuners;
+    a.K = c.grid.n_arms;
+    a.n_traces = c.n_traces;
+    a.t0 = t0;
+    a.n_steps = n_steps;
+    a.median_window = c.policy.median_window;
+    a.record_slots = c.record_slots;
+    a.prune_enable = c.prune.enable;
+    a.ext_L = c.prune.extreme_round_limit;
+    a.ext_n = c.prune.extreme_min_samples;
+    a.hist_t = c.prune.historical_min_round;
+    a.hist_n = c.prune.historical_min_samples;
+    a.f_min_mhz = c.grid.f_min_mhz;
+    a.f_step_mhz = c.grid.f_step_mhz;
+    a.tau = c.policy.tau;
+    a.clip_lo = c.policy.clip_lo;
+    a.clip_hi = c.policy.clip_hi;
+    a.tie_rel = c.policy.tie_rel;
+    // ENV.md §4.8: (double)F_k < cascade_fraction * (double)f_max_hw — one IEEE product
+    volatile double cf = c.prune.cascade_fraction;
+    a.cascade_limit = cf * (double)c.grid.f_max_hw_mhz;
+    a.W = c.env.window_s;
+    a.p_idle = c.env.p_idle;
+    a.u_floor = c.env.u_floor;
+    a.u_max = c.env.u_max;
+    return a;
+}
+
+}  // namespace
+
+extern "C" {
+
+agft_status agft_validate(const agft_config *cfg) { return validate(cfg); }
+
+uint32_t agft_struct_size(int which)
+{
+    switch (which) {
+    case 0: return (uint32_t)sizeof(agft_config);
+    case 1: return (uint32_t)sizeof(agft_tuner_params);
+    case 2: return (uint32_t)sizeof(agft_tuner_stats);
+    default: return 0;
+    }
+}
+
+size_t agft_workspace_bytes(const agft_config *cfg)
+{
+    if (validate(cfg) != AGFT_OK) return 0;
+    return make_layout(cfg->n_tuners, cfg->d).total;
+}
+
+agft_status agft_create(const agft_config *cfg, const agft_tuner_params *d_params, void *d_workspace,
+                        size_t ws_bytes, void *stream, agft_handle *out)
+{
+    if (!out) return AGFT_E_INVALID_ARG;
+    *out = nullptr;
+    agft_status st = validate(cfg);
+    if (st != AGFT_OK) return st;
+    if (!d_params || !d_workspace) return AGFT_E_INVALID_ARG;
+    if (reinterpret_cast<uintptr_t>(d_workspace) % 256 != 0) return AGFT_E_WORKSPACE;
+    const Layout L = make_layout(cfg->n_tuners, cfg->d);
+    if (ws_bytes < L.total) return AGFT_E_WORKSPACE;
+
+    int dev = 0, major = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return AGFT_E_DEVICE;
+    if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess) return AGFT_E_DEVICE;
+    if (major != 10) return AGFT_E_DEVICE;
+
+    agft_handle h = new (std::nothrow) agft_handle_s;
+    if (!h) return AGFT_E_INVALID_ARG;
+    h->cfg = *cfg;
+    h->layout = L;
+    h->ws = make_ws(d_workspace, L);
+    h->stream = static_cast<cudaStream_t>(stream);
+    h->t = 0;
+    h->sticky = AGFT_OK;
+
+    cudaError_t e = cudaMemcpyAsync(h->ws.params, d_params, sizeof(agft_tuner_params) * cfg->n_tuners,
+                                    cudaMemcpyDeviceToDevice, h->stream);
+    if (e == cudaSuccess) e = launch_init(h->ws, *cfg, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) {
+        delete h;
+        return AGFT_E_CUDA;
+    }
+    *out = h;
+    return AGFT_OK;
+}
+
+agft_status agft_reset(agft_handle h)
+{
+    if (!h) return AGFT_E_INVALID_ARG;
+    if (h->sticky != AGFT_OK) return h->sticky;
+    agft_status st = cuda_status(h, launch_init(h->ws, h->cfg, h->stream));
+    if (st == AGFT_OK) h->t = 0;
+    return st;
+}
+
+agft_status agft_trace_generate(agft_handle h, uint32_t t0, uint32_t n_steps, void *d_records, uint32_t *d_raw)
+{
+    if (!h || !d_records) return AGFT_E_INVALID_ARG;
+    if (h->sticky != AGFT_OK) return h->sticky;
+    const agft_config &c = h->cfg;
+    TraceArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.tc = c.trace;
+    a.env = c.env;
+    std::memcpy(a.norm_lo, c.norm_lo, sizeof(a.norm_lo));
+    std::memcpy(a.norm_hi, c.norm_hi, sizeof(a.norm_hi));
+    a.seed = c.env_seed;
+    a.trace_base = c.trace_base;
+    a.n_traces = c.n_traces;
+    a.t0 = t0;
+    a.n_steps = n_steps;
+    a.cap = c.trace.cap;
+    a.f_max_hw_mhz = c.grid.f_max_hw_mhz;
+    a.envc = h->ws.env;
+    a.records = static_cast<StepRec *>(d_records);
+    a.raw = d_raw;
+    return cuda_status(h, launch_trace(a, h->stream));
+}
+
+agft_status agft_replay(agft_handle h, const void *d_records, uint32_t t0, uint32_t n_steps, uint8_t *d_traj,
+                        double *d_gap)
+{
+    if (!h || !d_records) return AGFT_E_INVALID_ARG;
+    if (h->sticky != AGFT_OK) return h->sticky;
+    if (t0 != h->t) return AGFT_E_STATE;
+    if (n_steps == 0) return AGFT_OK;
+    ReplayArgs a = replay_args(h, d_records, t0, n_steps);
+    a.traj = h->cfg.record_slots ? d_traj : nullptr;
+    a.gap = h->cfg.record_slots ? d_gap : nullptr;
+    agft_status st = cuda_status(h, launch_replay(a, h->cfg.d, h->stream));
+    if (st == AGFT_OK) h->t += n_steps;
+    return st;
+}
+
+agft_status agft_step(agft_handle h, const void *d_records, uint32_t *d_chosen)
+{
+    if (!h || !d_records) return AGFT_E_INVALID_ARG;
+    if (h->sticky != AGFT_OK) return h->sticky;
+    ReplayArgs a = replay_args(h, d_records, h->t, 1);
+    a.chosen = d_chosen;
+    agft_status st = cuda_status(h, launch_replay(a, h->cfg.d, h->stream));
+    if (st == AGFT_OK) h->t += 1;
+    return st;
+}
+
+agft_status agft_stats(agft_handle h, agft_tuner_stats *d_out)
+{
+    if (!h || !d_out) return AGFT_E_INVALID_ARG;
+    if (h->sticky != AGFT_OK) return h->sticky;
+    return cuda_status(h, cudaMemcpyAsync(d_out, h->ws.acc, sizeof(agft_tuner_stats) * h->cfg.n_tuners,
+                                          cudaMemcpyDeviceToDevice, h->stream));
+}
+
+agft_status agft_export_arms(agft_handle h, uint32_t tuner, double *d_ainv_packed, double *d_b, double *d_theta,
+                             uint32_t *d_n, double *d_rbar, double *d_ebar, uint32_t *d_active_mask)
+{
+    if (!h) return AGFT_E_INVALID_ARG;
+    if (h->sticky != AGFT_OK) return h->sticky;
+    if (tuner >= h->cfg.n_tuners) return AGFT_E_INVALID_ARG;
+    return cuda_status(h, launch_export(h->ws, tuner, h->cfg.grid.n_arms, h->cfg.d, d_ainv_packed, d_b, d_theta,
+                                        d_n, d_rbar, d_ebar, d_active_mask, h->stream));
+}
+
+agft_status agft_get_step(agft_handle h, uint32_t *t)
+{
+    if (!h || !t) return AGFT_E_INVALID_ARG;
+    *t = h->t;
+    return AGFT_OK;
+}
+
+agft_status agft_run(const agft_config *cfg, const agft_tuner_params *h_params, agft_tuner_params *d_params_buf,
+                     uint32_t n_steps, uint32_t chunk_steps, void *d_workspace, size_t ws_bytes, void *d_scratch,
+                     size_t scratch_bytes, agft_tuner_stats *d_stats_buf, agft_tuner_stats *h_stats, void *stream)
+{
+    agft_status st = validate(cfg);
+    if (st != AGFT_OK) return st;
+    if (!h_params || !d_params_buf || !d_scratch || !d_stats_buf || !h_stats || chunk_steps == 0)
+        return AGFT_E_INVALID_ARG;
+    if (scratch_bytes < (size_t)cfg->n_traces * chunk_steps * AGFT_RECORD_BYTES) return AGFT_E_WORKSPACE;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (cudaMemcpyAsync(d_params_buf, h_params, sizeof(agft_tuner_params) * cfg->n_tuners, cudaMemcpyHostToDevice,
+                        s) != cudaSuccess)
+        return AGFT_E_CUDA;
+    agft_handle h = nullptr;
+    st = agft_create(cfg, d_params_buf, d_workspace, ws_bytes, stream, &h);
+    if (st != AGFT_OK) return st;
+    for (uint32_t t0 = 0; t0 < n_steps && st == AGFT_OK; t0 += chunk_steps) {
+        const uint32_t n = (n_steps - t0) < chunk_steps ? (n_steps - t0) : chunk_steps;
+        st = agft_trace_generate(h, t0, n, d_scratch, nullptr);
+        if (st == AGFT_OK) st = agft_replay(h, d_scratch, t0, n, nullptr, nullptr);
+    }
+    if (st == AGFT_OK) st = agft_stats(h, d_stats_buf);
+    if (st == AGFT_OK &&
+        cudaMemcpyAsync(h_stats, d_stats_buf, sizeof(agft_tuner_stats) * cfg->n_tuners, cudaMemcpyDeviceToHost,
+                        s) != cudaSuccess)
+        st = AGFT_E_CUDA;
+    if (st == AGFT_OK && cudaStreamSynchronize(s) != cudaSuccess) st = AGFT_E_CUDA;
+    agft_destroy(h);
+    return st;
+}
+
+agft_status agft_destroy(agft_handle h)
+{
+    if (!h) return AGFT_E_INVALID_ARG;
+    delete h;
+    return AGFT_OK;
+}
+
+const char *agft_status_string(agft_status s)
+{
+    switch (s) {
+    case AGFT_OK: return "ok";
+    case AGFT_E_INVALID_ARG: return "invalid argument";
+    case AGFT_E_INVALID_GRID: return "invalid frequency grid";
+    case AGFT_E_EMPTY_ARMS: return "empty arm set";
+    case AGFT_E_DIM: return "context dimension out of range";
+    case AGFT_E_NONFINITE: return "non-finite or out-of-range coefficient";
+    case AGFT_E_WORKSPACE: return "workspace too small or misaligned";
+    case AGFT_E_STATE: return "step counter mismatch";
+    case AGFT_E_CUDA: return "CUDA error";
+    case AGFT_E_DEVICE: return "no sm_100 device";
+    default: return "unknown status";
+    }
+}
+
+}  // extern "C"

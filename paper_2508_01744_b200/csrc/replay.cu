@@ -1,0 +1,497 @@
+// replay.cu — K2: the fused tuner step loop (rows a1–a11), one warp per tuner.
+//
+// Per step (PAPER §4.2–4.3, ENV.md §4):  record → α_t → Eq. 1 score of every
+// active arm → lexicographic (s desc, k asc) warp argmax → ENV-R response →
+// EDP-median reward → Sherman–Morrison update of the chosen arm (Eqs. 3–5) →
+// extreme / historical / cascade pruning → stats.
+//
+// Mapping: arm k lives in lane k%32, slot k/32 (S = ceil(K/32) ≤ 4 slots per lane).
+// Packed A⁻¹ and θ of every slot stay resident in shared memory across all steps
+// of the launch ([slot][entry][lane], conflict-free 8-byte accesses); n, r̄, ē and
+// the scores live in registers.  The 64-entry EDP window is spread 2 per lane
+// (sorted copy + chronological ring) and maintained with ballots and shuffles.
+// The canonical 128-slot reduction of ENV.md §4.8 maps onto this layout exactly:
+// levels 1–5 are the xor-butterfly across lanes (adjacent arms are adjacent lanes),
+// levels 6–7 combine the four slot partials in-lane.
+#include "agft_internal.cuh"
+
+namespace agft {
+
+namespace {
+
+constexpr double kInf = __builtin_huge_val();
+
+template <int S, typename T>
+__device__ __forceinline__ T pick(const T (&v)[S], int j)
+{
+    T r = v[0];
+#pragma unroll
+    for (int i = 1; i < S; ++i)
+        if (j == i) r = v[i];
+    return r;
+}
+
+template <int S, typename T>
+__device__ __forceinline__ void put(T (&v)[S], int j, T x)
+{
+#pragma unroll
+    for (int i = 0; i < S; ++i)
+        if (j == i) v[i] = x;
+}
+
+// canonical pairwise sum over 128 arm slots (ENV.md §4.8): value of arm 32*j + lane in v[j]
+template <int S>
+__device__ __forceinline__ double tree128(const double (&v)[S])
+{
+    double part[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int j = 0; j < S; ++j) {
+        double s = v[j];
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) s = xadd(s, __shfl_xor_sync(kFull, s, off));
+        part[j] = s;
+    }
+    return xadd(xadd(part[0], part[1]), xadd(part[2], part[3]));
+}
+
+__device__ __forceinline__ int popc_ballot(bool p) { return __popc(__ballot_sync(kFull, p)); }
+
+// ---- the 64-entry EDP window: sorted S[0..63] with S[2l], S[2l+1] in lane l (+inf padded)
+__device__ __forceinline__ double window_at(double lo, double hi, uint32_t idx)
+{
+    const double v = (idx & 1u) ? hi : lo;
+    return __shfl_sync(kFull, v, idx >> 1);
+}
+
+__device__ __forceinline__ void window_remove(double &lo, double &hi, double old, int lane)
+{
+    const int po = popc_ballot(lo < old) + popc_ballot(hi < old);
+    double nxt = __shfl_down_sync(kFull, lo, 1);
+    if (lane == 31) nxt = kInf;
+    const double nlo = (2 * lane < po) ? lo : hi;
+    const double nhi = (2 * lane + 1 < po) ? hi : nxt;
+    lo = nlo;
+    hi = nhi;
+}
+
+__device__ __forceinline__ void window_insert(double &lo, double &hi, double v, int lane)
+{
+    const int pi = popc_ballot(lo < v) + popc_ballot(hi < v);
+    const double prv = __shfl_up_sync(kFull, hi, 1);
+    const double nlo = (2 * lane < pi) ? lo : ((2 * lane == pi) ? v : prv);
+    const double nhi = (2 * lane + 1 < pi) ? hi : ((2 * lane + 1 == pi) ? v : lo);
+    lo = nlo;
+    hi = nhi;
+}
+
+constexpr int kWarpsPerBlock = 2;
+
+}  // namespace
+
+template <int D, int S>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+replay_kernel(const __grid_constant__ ReplayArgs a)
+{
+    constexpr int P = D * (D + 1) / 2;
+    extern __shared__ double smem[];
+    double *s_dec = smem, *s_pre = smem + kMaxArms, *s_pw = smem + 2 * kMaxArms;
+    const EnvConsts *ec = a.w.env;
+    for (int i = threadIdx.x; i < kMaxArms; i += blockDim.x) {
+        s_dec[i] = ec->dec[i];
+        s_pre[i] = ec->pre[i];
+        s_pw[i] = ec->pw[i];
+    }
+    __syncthreads();
+    const double invW = ec->invW, q_over = ec->q_over;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t tuner = blockIdx.x * kWarpsPerBlock + warp;
+    if (tuner >= a.n_tuners) return;
+    const uint64_t tb = tuner;
+    agft_tuner_stats st = a.w.acc[tb];
+    if (st.flags & 1u) return;                        // frozen by an earlier anomaly
+
+    double *sA = smem + 3 * kMaxArms + (size_t)warp * S * (P + D) * 32;
+    double *sT = sA + S * P * 32;
+    const agft_tuner_params prm = a.w.params[tb];
+    const uint32_t K = a.K;
+
+    // ---- load resident state
+    uint32_t n[S];
+    double rbar[S], ebar[S];
+    uint32_t act = 0;                                 // bit j: arm 32j+lane active
+#pragma unroll
+    for (int j = 0; j < S; ++j) {
+        const uint32_t k = 32u * j + lane;
+#pragma unroll
+        for (int e = 0; e < P; ++e) sA[(j * P + e) * 32 + lane] = a.w.ainv[(tb * P + e) * kMaxArms + k];
+#pragma unroll
+        for (int i = 0; i < D; ++i) sT[(j * D + i) * 32 + lane] = a.w.theta[(tb * D + i) * kMaxArms + k];
+        n[j] = a.w.n[tb * kMaxArms + k];
+        rbar[j] = a.w.rbar[tb * kMaxArms + k];
+        ebar[j] = a.w.ebar[tb * kMaxArms + k];
+        if (k < K && ((a.w.active[tb * 4 + j] >> lane) & 1u)) act |= 1u << j;
+    }
+    double wlo = a.w.wsorted[tb * kWindow + 2 * lane], whi = a.w.wsorted[tb * kWindow + 2 * lane + 1];
+    double rlo = a.w.wring[tb * kWindow + 2 * lane], rhi = a.w.wring[tb * kWindow + 2 * lane + 1];
+    uint32_t wcount = a.w.wmeta[tb * 2], whead = a.w.wmeta[tb * 2 + 1];
+    const uint32_t M = a.median_window;
+
+    const StepRec *rp = a.records + (size_t)prm.trace_id * a.n_steps;
+    double *bglob = a.w.b + tb * D * kMaxArms;
+
+    for (uint32_t s = 0; s < a.n_steps; ++s) {
+        const uint32_t t = a.t0 + s;
+        const StepRec &rec = rp[s];
+        double x[D];
+#pragma unroll
+        for (int i = 0; i < D; ++i) x[i] = rec.x[i];
+        const double g = rec.g, invIm = rec.invIm, invAm = rec.invAm, wIm = rec.wIm;
+        const double nT = rec.nT, nE = rec.nE, baseE = rec.baseE, baseEDP = rec.baseEDP;
+        const uint32_t recI = rec.I, recP = rec.P;
+
+        int nact = 0;
+#pragma unroll
+        for (int j = 0; j < S; ++j) nact += popc_ballot((act >> j) & 1u);
+
+        // ---- a3: α_t = α0/√(1+t/τ)
+        const double alpha = prm.alpha0 / sqrt(1.0 + (double)t / a.tau);
+
+        // ---- a4: Eq. 1 scores.  q = Σ_{i≤j} w_ij A⁻¹_ij with w_ij = x_i x_j (×2 off-diagonal)
+        double w[P];
+        {
+            int e = 0;
+#pragma unroll
+            for (int r = 0; r < D; ++r)
+#pragma unroll
+                for (int c = r; c < D; ++c, ++e) w[e] = (r == c) ? x[r] * x[r] : 2.0 * x[r] * x[c];
+        }
+        double sc[S], mg[S];
+        double bs = -kInf;
+        int bk = 0x7fffffff;
+#pragma unroll
+        for (int j = 0; j < S; ++j) {
+            sc[j] = -kInf;
+            mg[j] = 0.0;
+            if (__ballot_sync(kFull, (act >> j) & 1u) == 0) continue;
+            if ((act >> j) & 1u) {
+                const double *Aj = sA + j * P * 32 + lane;
+                const double *Tj = sT + j * D * 32 + lane;
+                double q = 0.0, p = 0.0;
+#pragma unroll
+                for (int e = 0; e < P; ++e) q = fma(w[e], Aj[e * 32], q);
+#pragma unroll
+                for (int i = 0; i < D; ++i) p = fma(Tj[i * 32], x[i], p);
+                const double bonus = alpha * sqrt(fmax(q, 0.0));   // AMB-19
+                sc[j] = p + bonus;
+                mg[j] = fabs(p) + bonus;
+                if (sc[j] > bs) { bs = sc[j]; bk = 32 * j + lane; }  // ascending k: ties keep lowest
+            }
+        }
+        // ---- a5/a6: lexicographic (s desc, k asc) warp argmax over F_available
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const double os = __shfl_xor_sync(kFull, bs, off);
+            const int ok = __shfl_xor_sync(kFull, bk, off);
+            if (os > bs || (os == bs && ok < bk)) { bs = os; bk = ok; }
+        }
+        const int kstar = bk, own = kstar & 31, jst = kstar >> 5;
+        const double sstar = bs;
+        const double mstar = __shfl_sync(kFull, pick<S>(mg, jst), own);
+        const bool fresh_star = __shfl_sync(kFull, pick<S>(n, jst) == 0u, own);
+
+        // ---- near-tie flag (ENV.md §4.5)
+        bool tie = false;
+        double s2 = -kInf, m2 = 0.0;
+#pragma unroll
+        for (int j = 0; j < S; ++j) {
+            if (!((act >> j) & 1u) || (32 * j + lane) == kstar) continue;
+            const double sc_ = fmax(mstar, mg[j]);
+            if (sstar - sc[j] < a.tie_rel * sc_ && !(fresh_star && n[j] == 0u)) tie = true;
+            if (sc[j] > s2) { s2 = sc[j]; m2 = mg[j]; }
+        }
+        const bool near = __ballot_sync(kFull, tie) != 0u;
+
+        // ---- a7: ENV-R response at f = f_min + k*·step (ENV.md §3.3), exact arithmetic
+        const double dec = s_dec[kstar], pre = s_pre[kstar], pw = s_pw[kstar];
+        const double t_dec = xmul((double)recI, dec);
+        const double t_pre = xmul((double)recP, pre);
+        const double busy = xmul(xadd(t_dec, t_pre), g);
+        const double u = xmul(busy, invW);
+        const double q = u <= a.u_max ? xdiv(1.0, xsub(1.0, u)) : xmul(u, q_over);
+        const double tpot = xmul(xmul(xmul(xadd(dec, xmul(t_pre, invIm)), g), q), nT);
+        double ue = u > 1.0 ? 1.0 : u;
+        ue = ue < a.u_floor ? a.u_floor : ue;
+        const double E = xmul(xmul(xadd(a.p_idle, xmul(pw, ue)), a.W), nE);
+        const double ttft = xmul(xadd(xmul(t_pre, invAm), xmul(t_dec, wIm)), q);
+        const double edp = xmul(E, tpot);
+
+        // ---- a8: reward = clip(1 − EDP/median(window)), then push EDP (AMB-3)
+        double r = 0.0;
+        if (wcount > 0) {
+            double ref;
+            if (wcount & 1u) {
+                ref = window_at(wlo, whi, wcount >> 1);
+            } else {
+                const double m0 = window_at(wlo, whi, (wcount >> 1) - 1), m1 = window_at(wlo, whi, wcount >> 1);
+                ref = xmul(xadd(m0, m1), 0.5);
+            }
+            r = xsub(1.0, xdiv(edp, ref));
+            r = r < a.clip_lo ? a.clip_lo : (r > a.clip_hi ? a.clip_hi : r);
+        }
+        if (!isfinite(edp) || !isfinite(r)) {         // anomaly: flag and freeze the tuner
+            st.flags |= 1u;
+            break;
+        }
+        uint32_t ri;
+        if (wcount < M) {
+            ri = wcount;
+            ++wcount;
+        } else {
+            const double old = window_at(rlo, rhi, whead);
+            window_remove(wlo, whi, old, lane);
+            ri = whead;
+            whead = (whead + 1 == M) ? 0u : whead + 1;
+        }
+        window_insert(wlo, whi, edp, lane);
+        if (lane == (int)(ri >> 1)) {
+            if (ri & 1u) rhi = edp; else rlo = edp;
+        }
+
+        // ---- a9: rank-1 update of the chosen arm (Eqs. 3–5) by its owner lane
+        if (lane == own) {
+            double *Aj = sA + jst * P * 32 + lane;
+            double *Tj = sT + jst * D * 32 + lane;
+            double Ap[P];
+#pragma unroll
+            for (int e = 0; e < P; ++e) Ap[e] = Aj[e * 32];
+            double z[D];
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+                double acc = 0.0;
+#pragma unroll
+                for (int c = 0; c < D; ++c) {
+                    const int lo = i < c ? i : c, hi = i < c ? c : i;
+                    acc = fma(Ap[lo * D - lo * (lo - 1) / 2 + (hi - lo)], x[c], acc);
+                }
+                z[i] = acc;
+            }
+            double xz = 0.0, px = 0.0;
+            double th[D];
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+                xz = fma(x[i], z[i], xz);
+                th[i] = Tj[i * 32];
+                px = fma(th[i], x[i], px);
+            }
+            const double invd = 1.0 / (1.0 + xz);              // Sherman–Morrison denominator
+            {
+                int e = 0;
+#pragma unroll
+                for (int r0 = 0; r0 < D; ++r0)
+#pragma unroll
+                    for (int c = r0; c < D; ++c, ++e) Aj[e * 32] = fma(-z[r0] * invd, z[c], Ap[e]);
+            }
+            const double coef = (r - px) * invd;                // RLS form of θ = A⁻¹ b (AMB-21)
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+                Tj[i * 32] = fma(z[i], coef, th[i]);
+                double *bp = bglob + (size_t)i * kMaxArms + kstar;
+                *bp = xadd(*bp, xmul(r, x[i]));                // b exact, as Eq. 4 writes it
+            }
+            const uint32_t nn = pick<S>(n, jst) + 1u;
+            const double inv = xdiv(1.0, (double)nn);
+            put<S>(n, jst, nn);
+            put<S>(rbar, jst, xadd(pick<S>(rbar, jst), xmul(xsub(r, pick<S>(rbar, jst)), inv)));
+            put<S>(ebar, jst, xadd(pick<S>(ebar, jst), xmul(xsub(edp, pick<S>(ebar, jst)), inv)));
+        }
+
+        // ---- a10: §4.3 pruning on the post-update state
+        if (a.prune_enable) {
+            bool ext[S], inq[S], hist[S];
+            int next = 0, nq = 0;
+#pragma unroll
+            for (int j = 0; j < S; ++j) {
+                const bool on = (act >> j) & 1u;
+                ext[j] = on && t < a.ext_L && n[j] >= a.ext_n && rbar[j] < prm.extreme_reward_threshold;
+                inq[j] = on && n[j] >= a.hist_n;
+                hist[j] = false;
+                next += popc_ballot(ext[j]);
+                nq += popc_ballot(inq[j]);
+            }
+            if (t >= a.hist_t && nq >= 2) {
+                double best = kInf;
+                double v[S], v2[S];
+#pragma unroll
+                for (int j = 0; j < S; ++j) {
+                    if (inq[j] && ebar[j] < best) best = ebar[j];
+                    v[j] = inq[j] ? ebar[j] : 0.0;
+                }
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) best = fmin(best, __shfl_xor_sync(kFull, best, off));
+                const double mu = xdiv(tree128<S>(v), (double)nq);
+#pragma unroll
+                for (int j = 0; j < S; ++j) {
+                    const double dv = xsub(ebar[j], mu);
+                    v2[j] = inq[j] ? xmul(dv, dv) : 0.0;
+                }
+                const double sd = xsqrt(xdiv(tree128<S>(v2), (double)nq));
+                const double thr = xadd(best, xmul(prm.historical_k, sd));
+                int nh = 0;
+#pragma unroll
+                for (int j = 0; j < S; ++j) {
+                    hist[j] = inq[j] && ebar[j] > thr;
+                    nh += popc_ballot(hist[j]);
+                }
+                next += nh;
+            }
+            if (next > 0) {
+                // cascade: all active arms below the highest removed arm under the limit
+                int kc = -1;
+#pragma unroll
+                for (int j = 0; j < S; ++j) {
+                    const uint32_t k = 32u * j + lane;
+                    const double F = (double)(a.f_min_mhz + k * a.f_step_mhz);
+                    if ((ext[j] || hist[j]) && F < a.cascade_limit) kc = (int)k;
+                }
+                kc = __reduce_max_sync(kFull, kc);
+                bool cas[S];
+                int remaining = 0;
+#pragma unroll
+                for (int j = 0; j < S; ++j) {
+                    const bool on = (act >> j) & 1u;
+                    const int k = 32 * j + lane;
+                    cas[j] = on && !ext[j] && !hist[j] && k < kc;
+                    remaining += popc_ballot(on && !ext[j] && !hist[j] && !cas[j]);
+                }
+                int restore = -1;
+                if (remaining == 0) {                   // AMB-11: keep the removed arm with max r̄
+                    double br = -kInf;
+                    int bkr = 0x7fffffff;
+#pragma unroll
+                    for (int j = 0; j < S; ++j)
+                        if ((ext[j] || hist[j] || cas[j]) && rbar[j] > br) { br = rbar[j]; bkr = 32 * j + lane; }
+#pragma unroll
+                    for (int off = 16; off > 0; off >>= 1) {
+                        const double ob = __shfl_xor_sync(kFull, br, off);
+                        const int ok = __shfl_xor_sync(kFull, bkr, off);
+                        if (ob > br || (ob == br && ok < bkr)) { br = ob; bkr = ok; }
+                    }
+                    restore = bkr;
+                }
+#pragma unroll
+                for (int j = 0; j < S; ++j) {
+                    const int k = 32 * j + lane;
+                    const bool rm = (ext[j] || hist[j] || cas[j]) && k != restore;
+                    const int ce = popc_ballot(rm && ext[j]);
+                    const int ch = popc_ballot(rm && !ext[j] && hist[j]);
+                    const int cc = popc_ballot(rm && !ext[j] && !hist[j]);
+                    st.n_pruned_extreme += ce;
+                    st.n_pruned_hist += ch;
+                    st.n_pruned_cascade += cc;
+                    if (rm) act &= ~(1u << j);
+                }
+            }
+        }
+
+        // ---- a11: stats (ENV.md §4.9 order) and trajectory record
+        st.sum_energy = xadd(st.sum_energy, E);
+        st.sum_tpot = xadd(st.sum_tpot, tpot);
+        st.sum_ttft = xadd(st.sum_ttft, ttft);
+        st.sum_edp = xadd(st.sum_edp, edp);
+        st.sum_reward = xadd(st.sum_reward, r);
+        st.base_energy = xadd(st.base_energy, baseE);
+        st.base_edp = xadd(st.base_edp, baseEDP);
+        st.traj_hash = (st.traj_hash ^ (uint64_t)kstar) * kFnvPrime;
+        st.sum_active += (uint64_t)nact;
+        st.steps += 1;
+        st.last_arm = (uint32_t)kstar;
+        st.near_tie_steps += near ? 1u : 0u;
+        if (a.traj && prm.record_slot != AGFT_NO_RECORD && lane == 0)
+            a.traj[(size_t)prm.record_slot * a.n_steps + s] = (uint8_t)kstar;
+        if (a.gap && prm.record_slot != AGFT_NO_RECORD) {
+            // relative top-2 gap: (s* − s2)/max(m*, m2), +inf when only one arm is active
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                const double os = __shfl_xor_sync(kFull, s2, off);
+                const double om = __shfl_xor_sync(kFull, m2, off);
+                if (os > s2) { s2 = os; m2 = om; }
+            }
+            if (lane == 0) {
+                const double den = fmax(mstar, m2);
+                a.gap[(size_t)prm.record_slot * a.n_steps + s] =
+                    (s2 == -kInf) ? kInf : (den > 0.0 ? (sstar - s2) / den : 0.0);
+            }
+        }
+        if (a.chosen && lane == 0) a.chosen[tb] = (uint32_t)kstar;
+    }
+
+    // ---- write back the resident state
+#pragma unroll
+    for (int j = 0; j < S; ++j) {
+        const uint32_t k = 32u * j + lane;
+#pragma unroll
+        for (int e = 0; e < P; ++e) a.w.ainv[(tb * P + e) * kMaxArms + k] = sA[(j * P + e) * 32 + lane];
+#pragma unroll
+        for (int i = 0; i < D; ++i) a.w.theta[(tb * D + i) * kMaxArms + k] = sT[(j * D + i) * 32 + lane];
+        a.w.n[tb * kMaxArms + k] = n[j];
+        a.w.rbar[tb * kMaxArms + k] = rbar[j];
+        a.w.ebar[tb * kMaxArms + k] = ebar[j];
+        const uint32_t bits = __ballot_sync(kFull, (act >> j) & 1u);
+        if (lane == 0) a.w.active[tb * 4 + j] = bits;
+    }
+    a.w.wsorted[tb * kWindow + 2 * lane] = wlo;
+    a.w.wsorted[tb * kWindow + 2 * lane + 1] = whi;
+    a.w.wring[tb * kWindow + 2 * lane] = rlo;
+    a.w.wring[tb * kWindow + 2 * lane + 1] = rhi;
+    int nact_end = 0;
+#pragma unroll
+    for (int j = 0; j < S; ++j) nact_end += popc_ballot((act >> j) & 1u);
+    if (lane == 0) {
+        a.w.wmeta[tb * 2] = wcount;
+        a.w.wmeta[tb * 2 + 1] = whead;
+        st.n_active = (uint32_t)nact_end;
+        a.w.acc[tb] = st;
+    }
+}
+
+template <int D, int S>
+static cudaError_t launch_ds(const ReplayArgs &a, cudaStream_t s)
+{
+    constexpr int P = D * (D + 1) / 2;
+    const size_t smem = (3 * kMaxArms + (size_t)kWarpsPerBlock * S * (P + D) * 32) * sizeof(double);
+    auto kern = replay_kernel<D, S>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const uint32_t blocks = (a.n_tuners + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    kern<<<blocks, kWarpsPerBlock * 32, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+template <int D>
+static cudaError_t launch_d(const ReplayArgs &a, cudaStream_t s)
+{
+    const uint32_t slots = (a.K + 31) / 32;
+    switch (slots) {
+    case 1: return launch_ds<D, 1>(a, s);
+    case 2: return launch_ds<D, 2>(a, s);
+    case 3: return launch_ds<D, 3>(a, s);
+    default: return launch_ds<D, 4>(a, s);
+    }
+}
+
+cudaError_t launch_replay(const ReplayArgs &a, uint32_t D, cudaStream_t s)
+{
+    if (a.n_tuners == 0 || a.n_steps == 0) return cudaSuccess;
+    switch (D) {
+    case 1: return launch_d<1>(a, s);
+    case 2: return launch_d<2>(a, s);
+    case 3: return launch_d<3>(a, s);
+    case 4: return launch_d<4>(a, s);
+    case 5: return launch_d<5>(a, s);
+    case 6: return launch_d<6>(a, s);
+    default: return launch_d<7>(a, s);
+    }
+}
+
+}  // namespace agft

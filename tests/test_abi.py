@@ -1,0 +1,124 @@
+"""CPU-side checks of the C-ABI boundary: the library builds and loads, exports every
+entry point include/agft.h declares, its struct mirrors match, and host validation
+returns the documented status codes. No kernel is launched here."""
+import math
+import os
+import re
+
+import pytest
+
+import paper_2508_01744_b200 as pkg
+from paper_2508_01744_b200 import _abi
+from agft_inputs import named_config
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "agft.h")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2508_01744_b200 import build
+    build.build()
+    return _abi.lib()
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(agft_[a-z_]+)\s*\(", src)))
+
+
+def test_header_declares_the_north_star_calls():
+    names = declared_functions()
+    for n in ("agft_create", "agft_step", "agft_replay", "agft_stats"):
+        assert n in names
+
+
+def test_library_exports_every_declared_symbol(lib):
+    names = declared_functions()
+    assert len(names) >= 12
+    for n in names:
+        assert hasattr(lib, n), n
+        assert n in _abi.PROTOTYPES, f"binding lacks {n}"
+
+
+def test_struct_mirrors_match(lib):
+    assert lib.agft_struct_size(0) == __import__("ctypes").sizeof(_abi.AgftConfig)
+    assert lib.agft_struct_size(1) == 32
+    assert lib.agft_struct_size(2) == 104
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5"])
+def test_named_configs_validate(lib, name):
+    c = _abi.make_config(named_config(name))
+    assert lib.agft_validate(c) == 0
+    assert pkg.agft_workspace_bytes(c) > 0
+
+
+def _bad(lib, **kw):
+    cfg = named_config("C2")
+    cfg.update(kw)
+    return lib.agft_validate(_abi.make_config(cfg))
+
+
+def test_validation_codes(lib):
+    assert _bad(lib, n_arms=0) == -3                         # S:161 empty arm set
+    assert _bad(lib, f_step_mhz=0) == -2                     # S:271 invalid grid
+    assert _bad(lib, n_arms=129) == -2
+    assert _bad(lib, n_arms=108) == -2                       # 210 + 107·15 > 1800
+    assert _bad(lib, d=0) == -4 and _bad(lib, d=8) == -4
+    assert _bad(lib, tau=math.nan) == -5                     # S:181 non-finite
+    assert _bad(lib, p_idle=-1.0) == -5
+    assert _bad(lib, u_max=1.0) == -5
+    assert _bad(lib, median_window=0) == -1 and _bad(lib, median_window=65) == -1
+    assert _bad(lib, weight=[1, 2, 3, 4, 5]) == -1
+    assert _bad(lib, norm_lo=[2.0] * 7) == -5                # lo > hi
+    c = _abi.make_config(named_config("C2"))
+    c.abi_version = 99
+    assert lib.agft_validate(c) == -1
+    c.abi_version = 1
+    c.n_tuners = 0
+    assert pkg.agft_workspace_bytes(c) == 0
+
+
+def test_workspace_scales_with_tuners(lib):
+    w1 = pkg.agft_workspace_bytes(_abi.make_config(named_config("C2"), n_tuners=1, n_traces=1))
+    w2 = pkg.agft_workspace_bytes(_abi.make_config(named_config("C2"), n_tuners=1000, n_traces=1))
+    assert w1 > 0 and w2 > 500 * w1
+    # ≈ 46 KB of resident tuner state at K=107 (padded to 128 arms), d=7
+    assert 40_000 < w2 / 1000 < 60_000
+
+
+def test_status_strings(lib):
+    for code, text in _abi.STATUS.items():
+        assert lib.agft_status_string(code).decode() == text
+
+
+def test_create_without_device_fails_cleanly(lib):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    import ctypes
+    import numpy as np
+    c = _abi.make_config(named_config("C1"))
+    buf = np.zeros(pkg.agft_workspace_bytes(c) + 256, np.uint8)
+    base = (buf.ctypes.data + 255) // 256 * 256
+    h = ctypes.c_void_p()
+    params = np.zeros(1, _abi.PARAMS_DTYPE)
+    rc = lib.agft_create(ctypes.byref(c), params.ctypes.data, base, buf.nbytes - 256, None, ctypes.byref(h))
+    assert rc in (-9, -8)
+
+
+def test_product_never_imports_the_oracle():
+    pdir = os.path.join(ROOT, "paper_2508_01744_b200")
+    for dirpath, _, files in os.walk(pdir):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert not re.search(r"\b(import|from)\s+oracle\b", txt), f
+                assert "agft_oracle" not in txt, f
+    for f in os.listdir(os.path.join(ROOT, "oracle")):
+        if f.endswith((".py", ".c", ".h")):
+            txt = open(os.path.join(ROOT, "oracle", f)).read()
+            assert not re.search(r"\b(import|from)\s+paper_2508_01744_b200\b", txt), f
+            assert not re.search(r'#include\s+"[^"]*(agft\.h|agft_internal)', txt), f

@@ -101,7 +101,7 @@ class TunerBatch:
     """N tuners on one GPU: owns (torch-allocated) workspace, params and the handle."""
 
     def __init__(self, cfg: dict, params: dict, device="cuda", record_slot=None, trace_base: int = 0,
-                 n_traces: int | None = None, stream=None):
+                 n_traces: int | None = None, stream=None, policy: int = 0):
         import torch
         self.cfg = cfg
         self.device = torch.device(device)
@@ -111,7 +111,7 @@ class TunerBatch:
             np.asarray(record_slot) == NO_RECORD, -1, record_slot)) + 1)
         self.record_slots = rec_slots
         self.cfg_c = make_config(cfg, n_tuners=self.n, n_traces=self.n_traces, trace_base=trace_base,
-                                 record_slots=rec_slots)
+                                 record_slots=rec_slots, policy=policy)
         ws = agft_workspace_bytes(self.cfg_c)
         if ws == 0:
             raise AgftError("agft_workspace_bytes", -1)

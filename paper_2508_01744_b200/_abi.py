@@ -55,7 +55,7 @@ class AgftTraceCfg(C.Structure):
 
 class AgftConfig(C.Structure):
     _fields_ = [("abi_version", u32), ("n_tuners", u32), ("d", u32), ("n_traces", u32),
-                ("trace_base", u32), ("record_slots", u32),
+                ("trace_base", u32), ("record_slots", u32), ("kernel_policy", u32), ("pad0", u32),
                 ("grid", AgftGrid), ("prune", AgftPrune), ("policy", AgftPolicy), ("env", AgftEnv),
                 ("trace", AgftTraceCfg), ("norm_lo", f64 * 7), ("norm_hi", f64 * 7), ("env_seed", u64)]
 
@@ -130,10 +130,11 @@ def check(fn: str, code: int):
 
 
 def make_config(cfg: dict, n_tuners: int | None = None, n_traces: int | None = None,
-                trace_base: int = 0, record_slots: int = 0) -> AgftConfig:
+                trace_base: int = 0, record_slots: int = 0, policy: int = 0) -> AgftConfig:
     """Marshal a named-config dict (agft_inputs.configs) into the C agft_config."""
     c = AgftConfig()
     c.abi_version = ABI_VERSION
+    c.kernel_policy = policy
     c.n_tuners = cfg["n_tuners"] if n_tuners is None else n_tuners
     c.d = cfg["d"]
     c.n_traces = cfg["n_traces"] if n_traces is None else n_traces

@@ -14,6 +14,8 @@ struct agft_handle_s {
     Layout layout;
     Ws ws;
     cudaStream_t stream;
+    cudaStream_t side[kNumCls];   // one stream per kernel class: classes of a sub-chunk overlap
+    cudaEvent_t fork, join[kNumCls];
     uint32_t t;             // current global step (observe/apply alternate strictly)
     agft_status sticky;     // AGFT_OK or AGFT_E_CUDA
 };
@@ -22,11 +24,31 @@ namespace {
 
 bool finite(double v) { return std::isfinite(v); }
 
+// Sub-chunk length between re-classifications: short while the action spaces are still
+// collapsing (most tuners reach K_act ≤ 32 within ~1,000 windows and K_act = 1 within
+// ~1,400), long once the classes are stable.
+uint32_t sub_chunk(uint32_t t)
+{
+    if (t < 2048) return 256;
+    if (t < 8192) return 1024;
+    return 4096;
+}
+
+void destroy_streams(agft_handle h)
+{
+    for (int c = 0; c < kNumCls; ++c) {
+        if (h->side[c]) cudaStreamDestroy(h->side[c]);
+        if (h->join[c]) cudaEventDestroy(h->join[c]);
+    }
+    if (h->fork) cudaEventDestroy(h->fork);
+}
+
 agft_status validate(const agft_config *c)
 {
     if (!c) return AGFT_E_INVALID_ARG;
     if (c->abi_version != AGFT_ABI_VERSION) return AGFT_E_INVALID_ARG;
     if (c->n_tuners == 0 || c->n_traces == 0) return AGFT_E_INVALID_ARG;
+    if (c->kernel_policy > AGFT_POLICY_WIDE) return AGFT_E_INVALID_ARG;
     const agft_grid &g = c->grid;
     if (g.n_arms == 0) return AGFT_E_EMPTY_ARMS;
     if (g.f_step_mhz == 0 || g.n_arms > AGFT_MAX_ARMS || g.f_min_mhz == 0) return AGFT_E_INVALID_GRID;
@@ -89,6 +111,8 @@ ReplayArgs replay_args(agft_handle h, const void *records, uint32_t t0, uint32_t
     a.n_traces = c.n_traces;
     a.t0 = t0;
     a.n_steps = n_steps;
+    a.rec_stride = n_steps;
+    a.rec_off = 0;
     a.median_window = c.policy.median_window;
     a.record_slots = c.record_slots;
     a.prune_enable = c.prune.enable;
@@ -159,12 +183,24 @@ agft_status agft_create(const agft_config *cfg, const agft_tuner_params *d_param
     h->stream = static_cast<cudaStream_t>(stream);
     h->t = 0;
     h->sticky = AGFT_OK;
+    h->fork = nullptr;
+    for (int c = 0; c < kNumCls; ++c) {
+        h->side[c] = nullptr;
+        h->join[c] = nullptr;
+    }
 
-    cudaError_t e = cudaMemcpyAsync(h->ws.params, d_params, sizeof(agft_tuner_params) * cfg->n_tuners,
-                                    cudaMemcpyDeviceToDevice, h->stream);
+    cudaError_t e = cudaEventCreateWithFlags(&h->fork, cudaEventDisableTiming);
+    for (int c = 0; c < kNumCls && e == cudaSuccess; ++c) {
+        e = cudaStreamCreateWithFlags(&h->side[c], cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->join[c], cudaEventDisableTiming);
+    }
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(h->ws.params, d_params, sizeof(agft_tuner_params) * cfg->n_tuners,
+                            cudaMemcpyDeviceToDevice, h->stream);
     if (e == cudaSuccess) e = launch_init(h->ws, *cfg, h->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
     if (e != cudaSuccess) {
+        destroy_streams(h);
         delete h;
         return AGFT_E_CUDA;
     }
@@ -205,6 +241,51 @@ agft_status agft_trace_generate(agft_handle h, uint32_t t0, uint32_t n_steps, vo
     return cuda_status(h, launch_trace(a, h->stream));
 }
 
+// The replay scheduler: steps [t0, t0+n) in sub-chunks; before each sub-chunk every tuner
+// is classified by its active-arm count and each class runs its kernel on its own stream.
+static agft_status run_steps(agft_handle h, const void *d_records, uint32_t t0, uint32_t n, uint8_t *traj,
+                             double *gap, uint32_t *chosen)
+{
+    const agft_config &c = h->cfg;
+    for (uint32_t s = 0; s < n;) {
+        const uint32_t t = t0 + s;
+        uint32_t len = sub_chunk(t);
+        if (len > n - s) len = n - s;
+        ReplayArgs a = replay_args(h, d_records, t, len);
+        a.rec_stride = n;
+        a.rec_off = s;
+        a.traj = c.record_slots ? traj : nullptr;
+        a.gap = c.record_slots ? gap : nullptr;
+        a.chosen = chosen;
+        cudaError_t e = cudaSuccess;
+        if (c.kernel_policy == AGFT_POLICY_WIDE) {
+            e = launch_replay(a, c.d, h->stream);
+        } else {
+            e = launch_classify(h->ws, c.n_tuners, h->stream);
+            if (e == cudaSuccess) e = cudaEventRecord(h->fork, h->stream);
+            for (int k = 0; k < kNumCls && e == cudaSuccess; ++k) {
+                ReplayArgs ak = a;
+                ak.list = h->ws.lists + (size_t)k * c.n_tuners;
+                ak.count = h->ws.counts + k;
+                e = cudaStreamWaitEvent(h->side[k], h->fork, 0);
+                if (e != cudaSuccess) break;
+                switch (k) {
+                case kClsWide: e = launch_replay(ak, c.d, h->side[k]); break;
+                case kClsSeg32: e = launch_seg(ak, c.d, 32, h->side[k]); break;
+                case kClsSeg16: e = launch_seg(ak, c.d, 16, h->side[k]); break;
+                case kClsSeg8: e = launch_seg(ak, c.d, 8, h->side[k]); break;
+                default: e = launch_solo(ak, c.d, h->side[k]); break;
+                }
+                if (e == cudaSuccess) e = cudaEventRecord(h->join[k], h->side[k]);
+                if (e == cudaSuccess) e = cudaStreamWaitEvent(h->stream, h->join[k], 0);
+            }
+        }
+        if (e != cudaSuccess) return cuda_status(h, e);
+        s += len;
+    }
+    return AGFT_OK;
+}
+
 agft_status agft_replay(agft_handle h, const void *d_records, uint32_t t0, uint32_t n_steps, uint8_t *d_traj,
                         double *d_gap)
 {
@@ -212,10 +293,7 @@ agft_status agft_replay(agft_handle h, const void *d_records, uint32_t t0, uint3
     if (h->sticky != AGFT_OK) return h->sticky;
     if (t0 != h->t) return AGFT_E_STATE;
     if (n_steps == 0) return AGFT_OK;
-    ReplayArgs a = replay_args(h, d_records, t0, n_steps);
-    a.traj = h->cfg.record_slots ? d_traj : nullptr;
-    a.gap = h->cfg.record_slots ? d_gap : nullptr;
-    agft_status st = cuda_status(h, launch_replay(a, h->cfg.d, h->stream));
+    agft_status st = run_steps(h, d_records, t0, n_steps, d_traj, d_gap, nullptr);
     if (st == AGFT_OK) h->t += n_steps;
     return st;
 }
@@ -224,9 +302,7 @@ agft_status agft_step(agft_handle h, const void *d_records, uint32_t *d_chosen)
 {
     if (!h || !d_records) return AGFT_E_INVALID_ARG;
     if (h->sticky != AGFT_OK) return h->sticky;
-    ReplayArgs a = replay_args(h, d_records, h->t, 1);
-    a.chosen = d_chosen;
-    agft_status st = cuda_status(h, launch_replay(a, h->cfg.d, h->stream));
+    agft_status st = run_steps(h, d_records, h->t, 1, nullptr, nullptr, d_chosen);
     if (st == AGFT_OK) h->t += 1;
     return st;
 }
@@ -290,6 +366,8 @@ agft_status agft_run(const agft_config *cfg, const agft_tuner_params *h_params, 
 agft_status agft_destroy(agft_handle h)
 {
     if (!h) return AGFT_E_INVALID_ARG;
+    cudaStreamSynchronize(h->stream);
+    destroy_streams(h);
     delete h;
     return AGFT_OK;
 }

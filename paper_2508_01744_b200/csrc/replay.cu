@@ -105,9 +105,10 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
     const double invW = ec->invW, q_over = ec->q_over;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t tuner = blockIdx.x * kWarpsPerBlock + warp;
-    if (tuner >= a.n_tuners) return;
-    const uint64_t tb = tuner;
+    const uint32_t widx = blockIdx.x * kWarpsPerBlock + warp;
+    const uint32_t cnt = a.count ? *a.count : a.n_tuners;
+    if (widx >= cnt) return;
+    const uint64_t tb = a.list ? a.list[widx] : widx;
     agft_tuner_stats st = a.w.acc[tb];
     if (st.flags & 1u) return;                        // frozen by an earlier anomaly
 
@@ -137,7 +138,7 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
     uint32_t wcount = a.w.wmeta[tb * 2], whead = a.w.wmeta[tb * 2 + 1];
     const uint32_t M = a.median_window;
 
-    const StepRec *rp = a.records + (size_t)prm.trace_id * a.n_steps;
+    const StepRec *rp = a.records + (size_t)prm.trace_id * a.rec_stride + a.rec_off;
     double *bglob = a.w.b + tb * D * kMaxArms;
 
     for (uint32_t s = 0; s < a.n_steps; ++s) {
@@ -408,7 +409,7 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
         st.last_arm = (uint32_t)kstar;
         st.near_tie_steps += near ? 1u : 0u;
         if (a.traj && prm.record_slot != AGFT_NO_RECORD && lane == 0)
-            a.traj[(size_t)prm.record_slot * a.n_steps + s] = (uint8_t)kstar;
+            a.traj[(size_t)prm.record_slot * a.rec_stride + a.rec_off + s] = (uint8_t)kstar;
         if (a.gap && prm.record_slot != AGFT_NO_RECORD) {
             // relative top-2 gap: (s* − s2)/max(m*, m2), +inf when only one arm is active
 #pragma unroll
@@ -419,7 +420,7 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
             }
             if (lane == 0) {
                 const double den = fmax(mstar, m2);
-                a.gap[(size_t)prm.record_slot * a.n_steps + s] =
+                a.gap[(size_t)prm.record_slot * a.rec_stride + a.rec_off + s] =
                     (s2 == -kInf) ? kInf : (den > 0.0 ? (sstar - s2) / den : 0.0);
             }
         }

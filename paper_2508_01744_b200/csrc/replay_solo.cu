@@ -1,0 +1,161 @@
+// replay_solo.cu — K2/SOLO: one LANE per tuner, for tuners whose action space has
+// collapsed to a single frequency (K_act = 1; 73% of C4's tuner-steps).
+//
+// With one active arm the argmax of Eq. 1 is that arm and pruning can change nothing
+// (the non-empty guard restores it, AMB-11), so a step is: ENV-R response → EDP-median
+// reward → Sherman–Morrison update (Eqs. 3–5) → Welford → stats, all per thread with no
+// cross-lane communication.  Arm state (A⁻¹, θ, b: 49 doubles at d = 7) lives in
+// registers for the whole launch; the sorted 64-entry EDP window lives in shared memory
+// ([entry][thread], conflict-free) and is maintained by one binary search plus an
+// insertion-sort walk from the evicted slot; the chronological ring stays in global
+// memory (one 8-byte read + write per step).
+#include "step_common.cuh"
+
+namespace agft {
+
+namespace {
+constexpr int kSoloThreads = 64;
+}
+
+template <int D>
+__global__ void __launch_bounds__(kSoloThreads) solo_kernel(const __grid_constant__ ReplayArgs a)
+{
+    constexpr int P = D * (D + 1) / 2;
+    __shared__ double S_[kWindow * kSoloThreads];
+    const uint32_t cnt = a.count ? *a.count : a.n_tuners;
+    const uint32_t i = blockIdx.x * kSoloThreads + threadIdx.x;
+    if (i >= cnt) return;                                        // no collectives below
+    const uint32_t tb = a.list ? a.list[i] : i;
+    double *S = S_ + threadIdx.x;                                // S[j * kSoloThreads]
+#define SW(j) S[(j) * kSoloThreads]
+
+    agft_tuner_stats st = a.w.acc[tb];
+    if (st.flags & 1u) return;
+    const agft_tuner_params prm = a.w.params[tb];
+    int k = 0;
+    {
+        const uint4 m = *reinterpret_cast<const uint4 *>(a.w.active + (size_t)tb * 4);
+        k = m.x ? __ffs(m.x) - 1 : m.y ? 31 + __ffs(m.y) : m.z ? 63 + __ffs(m.z) : 95 + __ffs(m.w);
+    }
+    double A[P], th[D], b[D];
+#pragma unroll
+    for (int e = 0; e < P; ++e) A[e] = a.w.ainv[((size_t)tb * P + e) * kMaxArms + k];
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+        th[r] = a.w.theta[((size_t)tb * D + r) * kMaxArms + k];
+        b[r] = a.w.b[((size_t)tb * D + r) * kMaxArms + k];
+    }
+    uint32_t n = a.w.n[(size_t)tb * kMaxArms + k];
+    double rbar = a.w.rbar[(size_t)tb * kMaxArms + k], ebar = a.w.ebar[(size_t)tb * kMaxArms + k];
+    const EnvConsts *ec = a.w.env;
+    const double dec = ec->dec[k], pre = ec->pre[k], pw = ec->pw[k], invW = ec->invW, q_over = ec->q_over;
+    for (int j = 0; j < kWindow; ++j) SW(j) = a.w.wsorted[(size_t)tb * kWindow + j];
+    uint32_t wcount = a.w.wmeta[(size_t)tb * 2], whead = a.w.wmeta[(size_t)tb * 2 + 1];
+    const uint32_t M = a.median_window;
+    double *ring = a.w.wring + (size_t)tb * kWindow;
+    const StepRec *rp = a.records + (size_t)prm.trace_id * a.rec_stride + a.rec_off;
+    const bool rec_on = prm.record_slot != AGFT_NO_RECORD;
+
+    double x[D];
+    RecView v;
+    load_rec<D>(rp, x, v);
+    for (uint32_t s = 0; s < a.n_steps; ++s) {
+        double xn[D];
+        RecView vn;
+        if (s + 1 < a.n_steps) load_rec<D>(rp + s + 1, xn, vn);   // prefetch the next window
+
+        // a7: response at the only active frequency
+        const Response o = env_response(dec, pre, pw, v.I, v.P, v.g, v.invIm, v.invAm, v.wIm, v.nT, v.nE,
+                                        invW, q_over, a.u_max, a.u_floor, a.p_idle, a.W);
+        // a8: reward against the median of the window, then push the EDP
+        double r = 0.0;
+        if (wcount > 0) {
+            const double ref = (wcount & 1u) ? SW(wcount >> 1)
+                                             : xmul(xadd(SW((wcount >> 1) - 1), SW(wcount >> 1)), 0.5);
+            r = reward_of(o.edp, ref, a.clip_lo, a.clip_hi);
+        }
+        if (!isfinite(o.edp) || !isfinite(r)) {
+            st.flags |= 1u;
+            break;
+        }
+        if (wcount < M) {
+            int j = (int)wcount;
+            while (j > 0 && SW(j - 1) > o.edp) { SW(j) = SW(j - 1); --j; }
+            SW(j) = o.edp;
+            ring[wcount] = o.edp;
+            ++wcount;
+        } else {
+            const double old = ring[whead];
+            int lo = 0, hi = (int)M;                       // lower_bound(old): S[lo] == old
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (SW(mid) < old) lo = mid + 1; else hi = mid;
+            }
+            int j = lo;
+            if (o.edp < old) {
+                while (j > 0 && SW(j - 1) > o.edp) { SW(j) = SW(j - 1); --j; }
+            } else {
+                while (j < (int)M - 1 && SW(j + 1) < o.edp) { SW(j) = SW(j + 1); ++j; }
+            }
+            SW(j) = o.edp;
+            ring[whead] = o.edp;
+            whead = (whead + 1 == M) ? 0u : whead + 1;
+        }
+        // a9: Eqs. 3–5 on the (only) chosen arm, Welford means
+        sm_update<D>(A, th, b, x, r);
+        welford(n, rbar, ebar, r, o.edp);
+        // a11
+        stats_add(st, o, r, v.baseE, v.baseEDP, k, 1u);
+        if (rec_on) {
+            if (a.traj) a.traj[(size_t)prm.record_slot * a.rec_stride + a.rec_off + s] = (uint8_t)k;
+            if (a.gap) a.gap[(size_t)prm.record_slot * a.rec_stride + a.rec_off + s] = kInf;
+        }
+        if (s + 1 < a.n_steps) {
+#pragma unroll
+            for (int q = 0; q < D; ++q) x[q] = xn[q];
+            v = vn;
+        }
+    }
+    if (a.chosen) a.chosen[tb] = (uint32_t)k;
+
+#pragma unroll
+    for (int e = 0; e < P; ++e) a.w.ainv[((size_t)tb * P + e) * kMaxArms + k] = A[e];
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+        a.w.theta[((size_t)tb * D + r) * kMaxArms + k] = th[r];
+        a.w.b[((size_t)tb * D + r) * kMaxArms + k] = b[r];
+    }
+    a.w.n[(size_t)tb * kMaxArms + k] = n;
+    a.w.rbar[(size_t)tb * kMaxArms + k] = rbar;
+    a.w.ebar[(size_t)tb * kMaxArms + k] = ebar;
+    for (int j = 0; j < kWindow; ++j) a.w.wsorted[(size_t)tb * kWindow + j] = SW(j);
+    a.w.wmeta[(size_t)tb * 2] = wcount;
+    a.w.wmeta[(size_t)tb * 2 + 1] = whead;
+    st.n_active = 1;
+    a.w.acc[tb] = st;
+#undef SW
+}
+
+template <int D>
+static cudaError_t launch_solo_d(const ReplayArgs &a, cudaStream_t s)
+{
+    const uint32_t blocks = (a.n_tuners + kSoloThreads - 1) / kSoloThreads;
+    solo_kernel<D><<<blocks, kSoloThreads, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_solo(const ReplayArgs &a, uint32_t D, cudaStream_t s)
+{
+    if (a.n_tuners == 0 || a.n_steps == 0) return cudaSuccess;
+    switch (D) {
+    case 1: return launch_solo_d<1>(a, s);
+    case 2: return launch_solo_d<2>(a, s);
+    case 3: return launch_solo_d<3>(a, s);
+    case 4: return launch_solo_d<4>(a, s);
+    case 5: return launch_solo_d<5>(a, s);
+    case 6: return launch_solo_d<6>(a, s);
+    default: return launch_solo_d<7>(a, s);
+    }
+}
+
+}  // namespace agft

@@ -1,0 +1,144 @@
+// step_common.cuh — per-step pieces shared by the replay kernels (WIDE / SEG / SOLO):
+// the ENV-R response, the reward clip, Welford and stats accumulation, all in the exact
+// IEEE arithmetic ENV.md §0 prescribes.
+#pragma once
+#include "agft_internal.cuh"
+
+namespace agft {
+
+constexpr double kInf = __builtin_huge_val();
+
+// ENV.md §3.3: response at the chosen frequency (per-arm constants dec/pre/pw).
+struct Response {
+    double E, tpot, ttft, edp;
+};
+
+__device__ __forceinline__ Response env_response(double dec, double pre, double pw, uint32_t I, uint32_t P,
+                                                 double g, double invIm, double invAm, double wIm, double nT,
+                                                 double nE, double invW, double q_over, double u_max,
+                                                 double u_floor, double p_idle, double W)
+{
+    Response o;
+    const double t_dec = xmul((double)I, dec);
+    const double t_pre = xmul((double)P, pre);
+    const double busy = xmul(xadd(t_dec, t_pre), g);
+    const double u = xmul(busy, invW);
+    const double q = u <= u_max ? xdiv(1.0, xsub(1.0, u)) : xmul(u, q_over);
+    o.tpot = xmul(xmul(xmul(xadd(dec, xmul(t_pre, invIm)), g), q), nT);
+    double ue = u > 1.0 ? 1.0 : u;
+    ue = ue < u_floor ? u_floor : ue;
+    o.E = xmul(xmul(xadd(p_idle, xmul(pw, ue)), W), nE);
+    o.ttft = xmul(xadd(xmul(t_pre, invAm), xmul(t_dec, wIm)), q);
+    o.edp = xmul(o.E, o.tpot);
+    return o;
+}
+
+// a8: r = clip(1 − EDP/ref) (AMB-3)
+__device__ __forceinline__ double reward_of(double edp, double ref, double lo, double hi)
+{
+    double r = xsub(1.0, xdiv(edp, ref));
+    return r < lo ? lo : (r > hi ? hi : r);
+}
+
+// Welford means with one reciprocal (ENV.md §4.7)
+__device__ __forceinline__ void welford(uint32_t &n, double &rbar, double &ebar, double r, double edp)
+{
+    n += 1u;
+    const double inv = xdiv(1.0, (double)n);
+    rbar = xadd(rbar, xmul(xsub(r, rbar), inv));
+    ebar = xadd(ebar, xmul(xsub(edp, ebar), inv));
+}
+
+// a11: stats in ENV.md §4.9 order
+__device__ __forceinline__ void stats_add(agft_tuner_stats &st, const Response &o, double r, double baseE,
+                                          double baseEDP, int kstar, uint32_t nact)
+{
+    st.sum_energy = xadd(st.sum_energy, o.E);
+    st.sum_tpot = xadd(st.sum_tpot, o.tpot);
+    st.sum_ttft = xadd(st.sum_ttft, o.ttft);
+    st.sum_edp = xadd(st.sum_edp, o.edp);
+    st.sum_reward = xadd(st.sum_reward, r);
+    st.base_energy = xadd(st.base_energy, baseE);
+    st.base_edp = xadd(st.base_edp, baseEDP);
+    st.traj_hash = (st.traj_hash ^ (uint64_t)kstar) * kFnvPrime;
+    st.sum_active += nact;
+    st.steps += 1u;
+    st.last_arm = (uint32_t)kstar;
+}
+
+// packed upper-triangle index of (r, c), r ≤ c, for a D×D symmetric matrix
+template <int D>
+__device__ __forceinline__ constexpr int pidx(int r, int c)
+{
+    return r * D - r * (r - 1) / 2 + (c - r);
+}
+
+// Sherman–Morrison update of one arm held in registers (Eqs. 3–5, AMB-21):
+// z = A⁻¹x, δ = 1 + xᵀz, A⁻¹ ← A⁻¹ − z zᵀ/δ, θ ← θ + z (r − θ·x)/δ, b ← b + r x (exact).
+template <int D>
+__device__ __forceinline__ void sm_update(double (&A)[D * (D + 1) / 2], double (&th)[D], double (&b)[D],
+                                          const double (&x)[D], double r)
+{
+    double z[D];
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        double acc = 0.0;
+#pragma unroll
+        for (int c = 0; c < D; ++c) acc = fma(A[i <= c ? pidx<D>(i, c) : pidx<D>(c, i)], x[c], acc);
+        z[i] = acc;
+    }
+    double xz = 0.0, px = 0.0;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        xz = fma(x[i], z[i], xz);
+        px = fma(th[i], x[i], px);
+    }
+    const double invd = 1.0 / (1.0 + xz);
+#pragma unroll
+    for (int r0 = 0; r0 < D; ++r0) {
+        const double zr = -z[r0] * invd;
+#pragma unroll
+        for (int c = r0; c < D; ++c) A[pidx<D>(r0, c)] = fma(zr, z[c], A[pidx<D>(r0, c)]);
+    }
+    const double coef = (r - px) * invd;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        th[i] = fma(z[i], coef, th[i]);
+        b[i] = xadd(b[i], xmul(r, x[i]));
+    }
+}
+
+// one record's fields, loaded once per step
+struct RecView {
+    double x[7];
+    double g, invIm, invAm, wIm, nT, nE, baseE, baseEDP;
+    uint32_t I, P;
+};
+
+template <int D>
+__device__ __forceinline__ void load_rec(const StepRec *__restrict__ p, double (&x)[D], RecView &v)
+{
+    const double2 *q = reinterpret_cast<const double2 *>(p);
+    double f[16];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const double2 t = __ldg(q + i);
+        f[2 * i] = t.x;
+        f[2 * i + 1] = t.y;
+    }
+#pragma unroll
+    for (int i = 0; i < D; ++i) x[i] = f[i];
+    v.g = f[7];
+    v.invIm = f[8];
+    v.invAm = f[9];
+    v.wIm = f[10];
+    v.nT = f[11];
+    v.nE = f[12];
+    v.baseE = f[13];
+    v.baseEDP = f[14];
+    const uint2 ip = *reinterpret_cast<const uint2 *>(&f[15]);
+    v.I = ip.x;
+    v.P = ip.y;
+}
+
+}  // namespace agft

@@ -27,7 +27,7 @@ def _cfg(name, **kw):
     return c
 
 
-def _run(cfg, T, ids=None, record=None, chunk=4500, params=None):
+def _run(cfg, T, ids=None, record=None, chunk=4500, params=None, policy=0):
     params = tuner_params(cfg, ids) if params is None else params
     n = len(params["trace_id"])
     rec_slot = None
@@ -35,7 +35,7 @@ def _run(cfg, T, ids=None, record=None, chunk=4500, params=None):
         rec_slot = np.full(n, NO_RECORD, np.uint32)
         for s, i in enumerate(record):
             rec_slot[i] = s
-    tb = TunerBatch(dict(cfg, n_tuners=n), params, device="cuda:0", record_slot=rec_slot)
+    tb = TunerBatch(dict(cfg, n_tuners=n), params, device="cuda:0", record_slot=rec_slot, policy=policy)
     traj, gap = tb.run(T, chunk=chunk, record=record is not None)
     st = tb.stats()
     return tb, params, st, traj, gap
@@ -90,18 +90,20 @@ def test_c1_parity():
     _check(cfg, tb, params, st, [0], 1000, traj)
 
 
-def test_c2_parity():
+@pytest.mark.parametrize("policy", [0, 1])
+def test_c2_parity(policy):
     cfg = _cfg("C2")
-    tb, params, st, traj, _ = _run(cfg, 4500, record=[0])
+    tb, params, st, traj, _ = _run(cfg, 4500, record=[0], policy=policy)
     _check(cfg, tb, params, st, [0], 4500, traj)
     assert st["n_active"][0] < 107                    # pruning really happened
 
 
 # ---------------------------------------------------------------- batches
-def test_c3_sampled_parity():
+@pytest.mark.parametrize("policy", [0, 1])
+def test_c3_sampled_parity(policy):
     cfg = _cfg("C3")
     sample = [0, 1, 31, 32, 33, 1000, 2047, 4094, 4095]
-    tb, params, st, traj, _ = _run(cfg, 4500, record=sample)
+    tb, params, st, traj, _ = _run(cfg, 4500, record=sample, policy=policy)
     _check(cfg, tb, params, st, sample, 4500, traj)
     assert np.all(st["steps"] == 4500) and np.all(st["flags"] == 0)
 
@@ -131,13 +133,14 @@ def test_c4_full_size_sampled_parity():
     dict(ext_round_limit=1000, ext_min_samples=1),    # extreme pruning + cascades
     dict(f_min_mhz=1200, n_arms=41),                  # no cascade region
 ])
-def test_edge_configs(kw):
+@pytest.mark.parametrize("policy", [0, 1])
+def test_edge_configs(kw, policy):
     cfg = _cfg("C2", n_tuners=5, n_traces=5, T=700)
     cfg.update(kw)
     ids = list(range(5))
     params = tuner_params(cfg, ids)
     params["alpha0"] = np.array([0.0, 0.3, 1.0, 2.0, 5.0])
-    tb, params, st, traj, _ = _run(cfg, 700, params=params, record=ids, chunk=256)
+    tb, params, st, traj, _ = _run(cfg, 700, params=params, record=ids, chunk=256, policy=policy)
     _check(cfg, tb, params, st, ids, 700, traj)
 
 
@@ -199,3 +202,19 @@ def test_invariants_on_gpu_state():
             m = rec["active_mask"][t - 1]
             k = int(traj[i][t])
             assert (m[k // 32] >> (k % 32)) & 1
+
+
+def test_scheduled_kernels_agree_with_wide_at_scale():
+    """All 4,096 C3 tuners: the class-scheduled kernels (WIDE → SEG → SOLO as arms are pruned)
+    reproduce the one-warp-per-tuner schedule bit for bit wherever neither flagged a near-tie."""
+    cfg = _cfg("C3")
+    _, _, sa, _, _ = _run(cfg, 4500, policy=0)
+    _, _, sw, _, _ = _run(cfg, 4500, policy=1)
+    ok = (sa["near_tie_steps"] == 0) & (sw["near_tie_steps"] == 0)
+    assert ok.mean() > 0.9
+    assert np.array_equal(sa["traj_hash"][ok], sw["traj_hash"][ok])
+    for f in ("sum_energy", "sum_edp", "sum_reward", "base_edp", "sum_active", "n_active"):
+        assert np.array_equal(sa[f][ok], sw[f][ok]), f
+    assert np.all(sa["steps"] == 4500) and np.all(sa["n_active"] >= 1)
+    # the schedule really exercised the narrow classes
+    assert (sa["n_active"] == 1).mean() > 0.5

@@ -121,6 +121,8 @@ def main():
     ap.add_argument("--T", type=int, default=None, help="override decision windows (debug only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--policy", type=int, default=int(os.environ.get("AGFT_POLICY", "0")),
+                    help="0 auto (SOLO/SEG/WIDE), 1 wide only, 2 SOLO/MSEG/WIDE")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -150,7 +152,7 @@ def main():
     n = cfg["n_tuners"]
     R = cfg["n_traces"]
     params = tuner_params(cfg)                        # local trace ids 0..R-1
-    tb = TunerBatch(cfg, params, device=f"cuda:{local}", trace_base=rank * R)
+    tb = TunerBatch(cfg, params, device=f"cuda:{local}", trace_base=rank * R, policy=args.policy)
     stream = torch.cuda.current_stream()
     chunk = min(CHUNK, T)
     records = tb.new_records(chunk)
@@ -253,7 +255,8 @@ def e2e_leg(cfg, params, rank, world, local, chunk, n, T, args) -> dict:
     import paper_2508_01744_b200 as pkg
     from paper_2508_01744_b200 import make_config, make_params, STATS_DTYPE
     dev = torch.device("cuda", local)
-    cfg_c = make_config(cfg, n_tuners=n, n_traces=cfg["n_traces"], trace_base=rank * cfg["n_traces"])
+    cfg_c = make_config(cfg, n_tuners=n, n_traces=cfg["n_traces"], trace_base=rank * cfg["n_traces"],
+                        policy=args.policy)
     ws = torch.empty(pkg.agft_workspace_bytes(cfg_c), dtype=torch.uint8, device=dev)
     scratch = torch.empty(cfg["n_traces"] * chunk * pkg.RECORD_BYTES, dtype=torch.uint8, device=dev)
     hp = torch.from_numpy(make_params(params).view(np.uint8)).pin_memory()

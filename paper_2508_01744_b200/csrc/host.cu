@@ -2,6 +2,7 @@
 // launches, status codes.  No device allocation happens here: every device buffer
 // is the caller's.
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 
@@ -34,6 +35,17 @@ uint32_t sub_chunk(uint32_t t)
     return 4096;
 }
 
+// lanes per tuner of the MSEG class (AGFT_MSEG_G ∈ {1, 2, 4, 8}; default 4)
+int mseg_g()
+{
+    static int g = [] {
+        const char *e = std::getenv("AGFT_MSEG_G");
+        const int v = e ? std::atoi(e) : 4;
+        return (v == 1 || v == 2 || v == 4 || v == 8) ? v : 4;
+    }();
+    return g;
+}
+
 void destroy_streams(agft_handle h)
 {
     for (int c = 0; c < kNumCls; ++c) {
@@ -48,7 +60,7 @@ agft_status validate(const agft_config *c)
     if (!c) return AGFT_E_INVALID_ARG;
     if (c->abi_version != AGFT_ABI_VERSION) return AGFT_E_INVALID_ARG;
     if (c->n_tuners == 0 || c->n_traces == 0) return AGFT_E_INVALID_ARG;
-    if (c->kernel_policy > AGFT_POLICY_WIDE) return AGFT_E_INVALID_ARG;
+    if (c->kernel_policy > AGFT_POLICY_MSEG) return AGFT_E_INVALID_ARG;
     const agft_grid &g = c->grid;
     if (g.n_arms == 0) return AGFT_E_EMPTY_ARMS;
     if (g.f_step_mhz == 0 || g.n_arms > AGFT_MAX_ARMS || g.f_min_mhz == 0) return AGFT_E_INVALID_GRID;
@@ -261,7 +273,8 @@ static agft_status run_steps(agft_handle h, const void *d_records, uint32_t t0, 
         if (c.kernel_policy == AGFT_POLICY_WIDE) {
             e = launch_replay(a, c.d, h->stream);
         } else {
-            e = launch_classify(h->ws, c.n_tuners, h->stream);
+            const bool split = c.kernel_policy != AGFT_POLICY_MSEG;
+            e = launch_classify(h->ws, c.n_tuners, split, h->stream);
             if (e == cudaSuccess) e = cudaEventRecord(h->fork, h->stream);
             for (int k = 0; k < kNumCls && e == cudaSuccess; ++k) {
                 ReplayArgs ak = a;
@@ -271,7 +284,7 @@ static agft_status run_steps(agft_handle h, const void *d_records, uint32_t t0, 
                 if (e != cudaSuccess) break;
                 switch (k) {
                 case kClsWide: e = launch_replay(ak, c.d, h->side[k]); break;
-                case kClsSeg32: e = launch_seg(ak, c.d, 32, h->side[k]); break;
+                case kClsSeg32: e = split ? launch_seg(ak, c.d, 32, h->side[k]) : launch_mseg(ak, c.d, mseg_g(), h->side[k]); break;
                 case kClsSeg16: e = launch_seg(ak, c.d, 16, h->side[k]); break;
                 case kClsSeg8: e = launch_seg(ak, c.d, 8, h->side[k]); break;
                 default: e = launch_solo(ak, c.d, h->side[k]); break;

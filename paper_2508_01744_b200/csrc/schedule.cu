@@ -10,12 +10,15 @@
 
 namespace agft {
 
-__device__ __forceinline__ int class_of(const Ws &w, uint32_t tb)
+// split: true  → WIDE (>32) / SEG32 / SEG16 / SEG8 / SOLO   (AGFT_POLICY_AUTO)
+//        false → WIDE (>32) / MSEG for 2..32 (in the SEG32 list) / SOLO   (AGFT_POLICY_MSEG)
+__device__ __forceinline__ int class_of(const Ws &w, uint32_t tb, bool split)
 {
     if (w.acc[tb].flags & 1u) return -1;                    // frozen: not scheduled
     const uint4 m = *reinterpret_cast<const uint4 *>(w.active + (size_t)tb * 4);
     const int k = __popc(m.x) + __popc(m.y) + __popc(m.z) + __popc(m.w);
     if (k <= 1) return kClsSolo;
+    if (!split && k <= 32) return kClsSeg32;
     if (k <= 8) return kClsSeg8;
     if (k <= 16) return kClsSeg16;
     if (k <= 32) return kClsSeg32;
@@ -23,13 +26,13 @@ __device__ __forceinline__ int class_of(const Ws &w, uint32_t tb)
 }
 
 // per-block counts of each class
-__global__ void __launch_bounds__(kPartBlock) class_count_kernel(Ws w, uint32_t N)
+__global__ void __launch_bounds__(kPartBlock) class_count_kernel(Ws w, uint32_t N, bool split)
 {
     __shared__ uint32_t cnt[kNumCls];
     if (threadIdx.x < kNumCls) cnt[threadIdx.x] = 0;
     __syncthreads();
     const uint32_t tb = blockIdx.x * kPartBlock + threadIdx.x;
-    const int c = tb < N ? class_of(w, tb) : -1;
+    const int c = tb < N ? class_of(w, tb, split) : -1;
 #pragma unroll
     for (int k = 0; k < kNumCls; ++k) {
         const uint32_t b = __ballot_sync(kFull, c == k);
@@ -54,11 +57,11 @@ __global__ void class_scan_kernel(Ws w, uint32_t nblk)
 }
 
 // stable scatter into the class lists
-__global__ void __launch_bounds__(kPartBlock) class_scatter_kernel(Ws w, uint32_t N)
+__global__ void __launch_bounds__(kPartBlock) class_scatter_kernel(Ws w, uint32_t N, bool split)
 {
     __shared__ uint32_t wcnt[kNumCls][kPartBlock / 32];
     const uint32_t tb = blockIdx.x * kPartBlock + threadIdx.x;
-    const int c = tb < N ? class_of(w, tb) : -1;
+    const int c = tb < N ? class_of(w, tb, split) : -1;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint32_t myrank = 0;
 #pragma unroll
@@ -75,12 +78,12 @@ __global__ void __launch_bounds__(kPartBlock) class_scatter_kernel(Ws w, uint32_
     }
 }
 
-cudaError_t launch_classify(const Ws &w, uint32_t N, cudaStream_t s)
+cudaError_t launch_classify(const Ws &w, uint32_t N, bool split, cudaStream_t s)
 {
     const uint32_t nblk = (N + kPartBlock - 1) / kPartBlock;
-    class_count_kernel<<<nblk, kPartBlock, 0, s>>>(w, N);
+    class_count_kernel<<<nblk, kPartBlock, 0, s>>>(w, N, split);
     class_scan_kernel<<<1, 32, 0, s>>>(w, nblk);
-    class_scatter_kernel<<<nblk, kPartBlock, 0, s>>>(w, N);
+    class_scatter_kernel<<<nblk, kPartBlock, 0, s>>>(w, N, split);
     return cudaGetLastError();
 }
 

@@ -108,6 +108,65 @@ __device__ __forceinline__ void sm_update(double (&A)[D * (D + 1) / 2], double (
     }
 }
 
+// ---- the sorted EDP window of ONE tuner in a strided shared-memory column (lane-private)
+// S[j * stride], j < 64, +inf padded; ring (chronological) in global memory.
+struct SmemWindow {
+    double *S;
+    int stride;
+    __device__ __forceinline__ double &at(int j) const { return S[j * stride]; }
+
+    __device__ __forceinline__ double median(uint32_t n) const
+    {
+        return (n & 1u) ? at(n >> 1) : xmul(xadd(at((n >> 1) - 1), at(n >> 1)), 0.5);
+    }
+    // insert into a window holding n < M values
+    __device__ __forceinline__ void insert(uint32_t n, double v) const
+    {
+        int j = (int)n;
+        while (j > 0 && at(j - 1) > v) { at(j) = at(j - 1); --j; }
+        at(j) = v;
+    }
+    // replace `old` (present) by v in a full window of M values: binary search, then an
+    // insertion-sort walk from the evicted slot toward v's position
+    __device__ __forceinline__ void replace(uint32_t M, double old, double v) const
+    {
+        int lo = 0, hi = (int)M;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (at(mid) < old) lo = mid + 1; else hi = mid;
+        }
+        int j = lo;
+        if (v < old) {
+            while (j > 0 && at(j - 1) > v) { at(j) = at(j - 1); --j; }
+        } else {
+            while (j < (int)M - 1 && at(j + 1) < v) { at(j) = at(j + 1); ++j; }
+        }
+        at(j) = v;
+    }
+};
+
+// a8 for a lane-private window: reward against the median of the window, then push edp
+__device__ __forceinline__ double reward_and_push(const SmemWindow &win, double *ring, uint32_t &wcount,
+                                                  uint32_t &whead, uint32_t M, double edp, double clip_lo,
+                                                  double clip_hi, bool &finite_ok)
+{
+    double r = 0.0;
+    if (wcount > 0) r = reward_of(edp, win.median(wcount), clip_lo, clip_hi);
+    finite_ok = isfinite(edp) && isfinite(r);
+    if (!finite_ok) return r;
+    if (wcount < M) {
+        win.insert(wcount, edp);
+        ring[wcount] = edp;
+        ++wcount;
+    } else {
+        const double old = ring[whead];
+        win.replace(M, old, edp);
+        ring[whead] = edp;
+        whead = (whead + 1 == M) ? 0u : whead + 1;
+    }
+    return r;
+}
+
 // one record's fields, loaded once per step
 struct RecView {
     double x[7];

@@ -90,7 +90,7 @@ def test_c1_parity():
     _check(cfg, tb, params, st, [0], 1000, traj)
 
 
-@pytest.mark.parametrize("policy", [0, 1])
+@pytest.mark.parametrize("policy", [0, 1, 2])
 def test_c2_parity(policy):
     cfg = _cfg("C2")
     tb, params, st, traj, _ = _run(cfg, 4500, record=[0], policy=policy)
@@ -99,7 +99,7 @@ def test_c2_parity(policy):
 
 
 # ---------------------------------------------------------------- batches
-@pytest.mark.parametrize("policy", [0, 1])
+@pytest.mark.parametrize("policy", [0, 1, 2])
 def test_c3_sampled_parity(policy):
     cfg = _cfg("C3")
     sample = [0, 1, 31, 32, 33, 1000, 2047, 4094, 4095]
@@ -133,7 +133,7 @@ def test_c4_full_size_sampled_parity():
     dict(ext_round_limit=1000, ext_min_samples=1),    # extreme pruning + cascades
     dict(f_min_mhz=1200, n_arms=41),                  # no cascade region
 ])
-@pytest.mark.parametrize("policy", [0, 1])
+@pytest.mark.parametrize("policy", [0, 1, 2])
 def test_edge_configs(kw, policy):
     cfg = _cfg("C2", n_tuners=5, n_traces=5, T=700)
     cfg.update(kw)
@@ -204,11 +204,12 @@ def test_invariants_on_gpu_state():
             assert (m[k // 32] >> (k % 32)) & 1
 
 
-def test_scheduled_kernels_agree_with_wide_at_scale():
+@pytest.mark.parametrize("policy", [0, 2])
+def test_scheduled_kernels_agree_with_wide_at_scale(policy):
     """All 4,096 C3 tuners: the class-scheduled kernels (WIDE → SEG → SOLO as arms are pruned)
     reproduce the one-warp-per-tuner schedule bit for bit wherever neither flagged a near-tie."""
     cfg = _cfg("C3")
-    _, _, sa, _, _ = _run(cfg, 4500, policy=0)
+    _, _, sa, _, _ = _run(cfg, 4500, policy=policy)
     _, _, sw, _, _ = _run(cfg, 4500, policy=1)
     ok = (sa["near_tie_steps"] == 0) & (sw["near_tie_steps"] == 0)
     assert ok.mean() > 0.9

@@ -123,7 +123,12 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--policy", type=int, default=int(os.environ.get("AGFT_POLICY", "0")),
                     help="0 auto (SOLO/SEG/WIDE), 1 wide only, 2 SOLO/MSEG/WIDE")
+    ap.add_argument("--scaling", default=None, choices=["weak", "strong"],
+                    help="weak: every rank runs the full config (default for C1-C4); strong: split it (C5)")
+    ap.add_argument("--backend", default="nccl", help="process-group backend for N > 1 (nccl; gloo for tests)")
     args = ap.parse_args()
+    if args.scaling is None:
+        args.scaling = "strong" if args.config == "C5" else "weak"
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -143,21 +148,28 @@ def main():
     import paper_2508_01744_b200 as pkg
     from paper_2508_01744_b200 import TunerBatch, STATS_DTYPE
 
+    from paper_2508_01744_b200 import shard
+    local = local % max(1, torch.cuda.device_count())   # >1 rank per GPU only for gloo smoke tests
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(args.backend)
 
-    n = cfg["n_tuners"]
-    R = cfg["n_traces"]
-    params = tuner_params(cfg)                        # local trace ids 0..R-1
-    tb = TunerBatch(cfg, params, device=f"cuda:{local}", trace_base=rank * R, policy=args.policy)
+    sh = shard.plan(cfg, world, rank, args.scaling)
+    n, R = sh.n_tuners, sh.n_traces
+    cfg = dict(cfg, n_tuners=n, n_traces=R)
+    params = sh.params                                # local trace ids 0..R-1
+    tb = TunerBatch(cfg, params, device=f"cuda:{local}", trace_base=sh.trace_base, policy=args.policy)
     stream = torch.cuda.current_stream()
     chunk = min(CHUNK, T)
     records = tb.new_records(chunk)
     stats_out = tb.stats_tensor()
-    gathered = (torch.empty(world * stats_out.numel(), dtype=torch.uint8, device=stats_out.device)
+    coll_dev = stats_out.device if args.backend == "nccl" else torch.device("cpu")
+    gathered = (torch.empty(world * stats_out.numel(), dtype=torch.uint8, device=coll_dev)
                 if world > 1 else None)
     n_chunks = (T + chunk - 1) // chunk
     ev_replay = []
@@ -179,7 +191,7 @@ def main():
             t += m
         pkg.agft_stats(tb.h, stats_out)
         if world > 1:
-            dist.all_gather_into_tensor(gathered, stats_out)
+            dist.all_gather_into_tensor(gathered, stats_out.to(coll_dev))
 
     for _ in range(args.warmup):
         one_step(False)
@@ -203,7 +215,7 @@ def main():
     ms = start.elapsed_time(end)
     replay_ms = sum(a.elapsed_time(b) for a, b in ev_replay)
     if world > 1:
-        t_ = torch.tensor([ms], dtype=torch.float64, device=stats_out.device)
+        t_ = torch.tensor([ms], dtype=torch.float64, device=coll_dev)
         dist.all_reduce(t_, op=dist.ReduceOp.MAX)
         ms = float(t_.item())
 
@@ -227,7 +239,7 @@ def main():
 
     out = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": {"workload": f"{args.config}: {n} tuners/GPU × {cfg['n_arms']} arms × d={cfg['d']} × "
                                   f"{T} windows ({R} traces/GPU, α×pruning sweep, diurnal+burst)",
                       "tuners_per_gpu": n, "T": T, "arms": cfg["n_arms"], "d": cfg["d"],
@@ -238,7 +250,7 @@ def main():
            "gpu_launches": args.steps * (2 + 2 * n_chunks), "all_steps_complete": steps_ok}
 
     if not args.no_e2e:
-        out["e2e"] = e2e_leg(cfg, params, rank, world, local, chunk, n, T, args)
+        out["e2e"] = e2e_leg(cfg, params, sh.trace_base, world, local, chunk, n, T, args)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = run_cpu_baseline(cfg, 256, T)
     if rank == 0:
@@ -247,15 +259,15 @@ def main():
         dist.destroy_process_group()
 
 
-def e2e_leg(cfg, params, rank, world, local, chunk, n, T, args) -> dict:
+def e2e_leg(cfg, params, trace_base, world, local, chunk, n, T, args) -> dict:
     """Same metric through agft_run with HOST params/stats: H2D of the per-tuner params and
     D2H of the per-tuner stats are inside the timed region, every step."""
     import numpy as np
     import torch
     import paper_2508_01744_b200 as pkg
     from paper_2508_01744_b200 import make_config, make_params, STATS_DTYPE
-    dev = torch.device("cuda", local)
-    cfg_c = make_config(cfg, n_tuners=n, n_traces=cfg["n_traces"], trace_base=rank * cfg["n_traces"],
+    dev = torch.device("cuda", local % max(1, torch.cuda.device_count()))
+    cfg_c = make_config(cfg, n_tuners=n, n_traces=cfg["n_traces"], trace_base=trace_base,
                         policy=args.policy)
     ws = torch.empty(pkg.agft_workspace_bytes(cfg_c), dtype=torch.uint8, device=dev)
     scratch = torch.empty(cfg["n_traces"] * chunk * pkg.RECORD_BYTES, dtype=torch.uint8, device=dev)
@@ -274,7 +286,7 @@ def e2e_leg(cfg, params, rank, world, local, chunk, n, T, args) -> dict:
     dt = time.perf_counter() - t
     if world > 1:
         import torch.distributed as dist
-        t_ = torch.tensor([dt], dtype=torch.float64, device=dev)
+        t_ = torch.tensor([dt], dtype=torch.float64, device=dev if args.backend == "nccl" else "cpu")
         dist.all_reduce(t_, op=dist.ReduceOp.MAX)
         dt = float(t_.item())
     return {"value": round(n * T * world * reps / dt, 1), "unit": UNIT, "h2d_bytes_per_step": hp.numel(),

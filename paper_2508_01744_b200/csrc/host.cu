@@ -284,9 +284,9 @@ static agft_status run_steps(agft_handle h, const void *d_records, uint32_t t0, 
                 if (e != cudaSuccess) break;
                 switch (k) {
                 case kClsWide: e = launch_replay(ak, c.d, h->side[k]); break;
-                case kClsSeg32: e = split ? launch_seg(ak, c.d, 32, h->side[k]) : launch_mseg(ak, c.d, mseg_g(), h->side[k]); break;
-                case kClsSeg16: e = launch_seg(ak, c.d, 16, h->side[k]); break;
-                case kClsSeg8: e = launch_seg(ak, c.d, 8, h->side[k]); break;
+                case kClsSeg32: e = split ? launch_seg2(ak, c.d, 16, h->side[k]) : launch_mseg(ak, c.d, mseg_g(), h->side[k]); break;
+                case kClsSeg16: e = launch_seg2(ak, c.d, 8, h->side[k]); break;
+                case kClsSeg8: e = launch_seg2(ak, c.d, 4, h->side[k]); break;
                 default: e = launch_solo(ak, c.d, h->side[k]); break;
                 }
                 if (e == cudaSuccess) e = cudaEventRecord(h->join[k], h->side[k]);

@@ -227,7 +227,8 @@ __global__ void __launch_bounds__(kMsegTunersPerBlock * G) mseg_kernel(const __g
         int ok = 1;
         if (l == 0 && live) {
             bool fin;
-            r = reward_and_push(win, ring, wcount, whead, M, o.edp, a.clip_lo, a.clip_hi, fin);
+            double oldest = ring_oldest(ring, wcount, whead, M);
+            r = reward_and_push(win, ring, wcount, whead, M, o.edp, a.clip_lo, a.clip_hi, fin, oldest);
             ok = fin ? 1 : 0;
         }
         r = __shfl_sync(kFull, r, 0, G);

@@ -1,0 +1,491 @@
+// replay_seg2.cu — K2/SEG<G>: G lanes per tuner (32/G tuners per warp), TWO compacted arms
+// per lane, for tuners with 2 ≤ K_act ≤ 2G active arms (G = 4, 8, 16 → K ≤ 8, 16, 32).
+//
+// Why two arms per lane: the per-tuner scalar work of a step (ENV-R response, reward
+// median, Sherman–Morrison, Welford, stats) is one warp instruction stream shared by the
+// 32/G tuners of a warp, so halving G halves its cost per tuner-step; scoring costs the same
+// lane-instructions either way.  Packed A⁻¹ of both slots lives in shared
+// memory ([warp][slot][entry][lane], conflict-free), θ/n/r̄/ē/key in registers, per-segment
+// stats in shared memory (lane 0 of the segment owns them), so registers stay low enough for
+// ~10–12 warps per SM.
+//
+// Arm order: lane l holds active-order arms j = l (slot 0) and j = G + l (slot 1), so keys
+// ascend along (slot, lane) and the lexicographic argmax compares (score desc, key asc).
+// The canonical 128-slot reduction of ENV.md §4.8: values are scattered to their arm slots
+// in a per-segment shared array, each lane reduces an aligned 128/G-slot block pairwise, and a
+// width-G butterfly combines the blocks — the same pairwise tree, empty slots adding +0.0.
+// Control flow is warp-uniform around every collective; per-segment effects are predicated.
+#include "step_common.cuh"
+
+namespace agft {
+
+namespace {
+
+constexpr int kSeg2Warps = 2;
+#ifndef AGFT_SEG2_MIN_BLOCKS
+#define AGFT_SEG2_MIN_BLOCKS 4          // no effective register cap: spills cost more than occupancy gains (A/B)
+#endif
+constexpr int kSeg2MinBlocks = AGFT_SEG2_MIN_BLOCKS;
+
+template <int G>
+__device__ __forceinline__ uint32_t sbits(bool p, int sg)
+{
+    const uint32_t b = __ballot_sync(kFull, p);
+    return G == 32 ? b : (b >> (sg * G)) & ((1u << G) - 1u);
+}
+template <int G>
+__device__ __forceinline__ int spopc(bool p, int sg) { return __popc(sbits<G>(p, sg)); }
+template <int G>
+__device__ __forceinline__ int sisum(int v)
+{
+#pragma unroll
+    for (int off = G / 2; off > 0; off >>= 1) v += __shfl_xor_sync(kFull, v, off, G);
+    return v;
+}
+
+// sorted window element idx (S[l*E + e] in lane l of the segment)
+template <int G, int E>
+__device__ __forceinline__ double wat(const double (&S)[E], uint32_t idx)
+{
+    double v = S[0];
+#pragma unroll
+    for (int e = 1; e < E; ++e)
+        if ((idx % E) == (uint32_t)e) v = S[e];
+    return __shfl_sync(kFull, v, idx / E, G);
+}
+template <int G, int E>
+__device__ __forceinline__ int wless(const double (&S)[E], double v)
+{
+    int c = 0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) c += (S[e] < v) ? 1 : 0;
+    return sisum<G>(c);
+}
+template <int G, int E>
+__device__ __forceinline__ void wremove(double (&S)[E], int po, int l)
+{
+    double nxt = __shfl_down_sync(kFull, S[0], 1, G);
+    if (l == G - 1) nxt = kInf;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const double up = (e + 1 < E) ? S[e + 1 < E ? e + 1 : e] : nxt;
+        S[e] = (l * E + e < po) ? S[e] : up;
+    }
+}
+template <int G, int E>
+__device__ __forceinline__ void winsert(double (&S)[E], double v, int pi, int l)
+{
+    const double prv = __shfl_up_sync(kFull, S[E - 1], 1, G);
+#pragma unroll
+    for (int e = E - 1; e >= 0; --e) {
+        const int i = l * E + e;
+        const double dn = (e > 0) ? S[e > 0 ? e - 1 : 0] : prv;
+        S[e] = (i < pi) ? S[e] : ((i == pi) ? v : dn);
+    }
+}
+
+// canonical tree: scatter (has0,key0,v0), (has1,key1,v1) of every lane to `buf` (128 zeros
+// on entry, restored to zeros on exit), reduce aligned blocks, butterfly
+template <int G>
+__device__ __forceinline__ double stree(double *buf, int l, bool h0, int k0, double v0, bool h1, int k1, double v1)
+{
+    constexpr int SL = 128 / G;
+    if (h0) buf[k0] = v0;
+    if (h1) buf[k1] = v1;
+    __syncwarp();
+    double v[SL];
+#pragma unroll
+    for (int j = 0; j < SL; ++j) v[j] = buf[l * SL + j];
+#pragma unroll
+    for (int len = SL; len > 1; len >>= 1)
+#pragma unroll
+        for (int j = 0; j < len / 2; ++j) v[j] = xadd(v[2 * j], v[2 * j + 1]);
+    double s = v[0];
+#pragma unroll
+    for (int off = 1; off < G; off <<= 1) s = xadd(s, __shfl_xor_sync(kFull, s, off, G));
+    __syncwarp();
+    if (h0) buf[k0] = 0.0;
+    if (h1) buf[k1] = 0.0;
+    __syncwarp();
+    return s;
+}
+
+template <int G>
+constexpr size_t seg2_smem_bytes(int P)
+{
+    return (3 * kMaxArms + (size_t)kSeg2Warps * 2 * P * 32 + (size_t)kSeg2Warps * (32 / G) * kMaxArms) * 8 +
+           (size_t)kSeg2Warps * (32 / G) * sizeof(agft_tuner_stats);
+}
+
+}  // namespace
+
+template <int D, int G>
+__global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(const __grid_constant__ ReplayArgs a)
+{
+    constexpr int P = D * (D + 1) / 2;
+    constexpr int E = kWindow / G;
+    constexpr int NSEG = 32 / G;
+    extern __shared__ double sm[];
+    double *s_dec = sm, *s_pre = sm + kMaxArms, *s_pw = sm + 2 * kMaxArms;
+    double *s_A = sm + 3 * kMaxArms;                                   // [warp][slot][P][32]
+    double *s_tree = s_A + kSeg2Warps * 2 * P * 32;                    // [warp][seg][128]
+    agft_tuner_stats *s_st = reinterpret_cast<agft_tuner_stats *>(s_tree + kSeg2Warps * NSEG * kMaxArms);
+    const EnvConsts *ec = a.w.env;
+    for (int q = threadIdx.x; q < kMaxArms; q += blockDim.x) {
+        s_dec[q] = ec->dec[q];
+        s_pre[q] = ec->pre[q];
+        s_pw[q] = ec->pw[q];
+    }
+    for (int q = threadIdx.x; q < kSeg2Warps * NSEG * kMaxArms; q += blockDim.x) s_tree[q] = 0.0;
+    __syncthreads();
+    const double invW = ec->invW, q_over = ec->q_over;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int sg = lane / G, l = lane % G;
+    const uint32_t cnt = a.count ? *a.count : a.n_tuners;
+    const uint32_t wbase = (blockIdx.x * kSeg2Warps + warp) * NSEG;
+    if (wbase >= cnt) return;                                         // warp-uniform
+    const uint32_t idx = wbase + sg;
+    const bool valid = idx < cnt;
+    const uint32_t tb = a.list ? a.list[valid ? idx : cnt - 1] : (valid ? idx : cnt - 1);
+    double *tree = s_tree + (warp * NSEG + sg) * kMaxArms;
+    double *A0 = s_A + (warp * 2 + 0) * P * 32 + lane;                 // slot 0 column
+    double *A1 = s_A + (warp * 2 + 1) * P * 32 + lane;                 // slot 1 column
+    agft_tuner_stats &st = s_st[warp * NSEG + sg];
+    if (l == 0) st = a.w.acc[tb];
+    __syncwarp();
+    bool live = valid && !(st.flags & 1u);
+    const agft_tuner_params prm = a.w.params[tb];
+
+    // ---- compact the active arms: lane l ← active-order arms l and G + l
+    int key0 = 0, key1 = 0;
+    bool act0 = false, act1 = false;
+    {
+        const uint4 m4 = *reinterpret_cast<const uint4 *>(a.w.active + (size_t)tb * 4);
+        const uint32_t mw[4] = {m4.x, m4.y, m4.z, m4.w};
+        int j = 0;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            uint32_t mm = mw[w];
+            while (mm) {
+                const int k = 32 * w + __ffs(mm) - 1;
+                mm &= mm - 1u;
+                if (j == l) { key0 = k; act0 = true; }
+                if (j == G + l) { key1 = k; act1 = true; }
+                ++j;
+            }
+        }
+    }
+    const bool has0 = act0, has1 = act1;                              // slots holding an arm
+    double th0[D], th1[D];
+    uint32_t n0 = 0, n1 = 0;
+    double rb0 = 0.0, rb1 = 0.0, eb0 = 0.0, eb1 = 0.0;
+#pragma unroll
+    for (int e = 0; e < P; ++e) {
+        A0[e * 32] = has0 ? a.w.ainv[((size_t)tb * P + e) * kMaxArms + key0] : 0.0;
+        A1[e * 32] = has1 ? a.w.ainv[((size_t)tb * P + e) * kMaxArms + key1] : 0.0;
+    }
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+        th0[r] = has0 ? a.w.theta[((size_t)tb * D + r) * kMaxArms + key0] : 0.0;
+        th1[r] = has1 ? a.w.theta[((size_t)tb * D + r) * kMaxArms + key1] : 0.0;
+    }
+    if (has0) {
+        n0 = a.w.n[(size_t)tb * kMaxArms + key0];
+        rb0 = a.w.rbar[(size_t)tb * kMaxArms + key0];
+        eb0 = a.w.ebar[(size_t)tb * kMaxArms + key0];
+    }
+    if (has1) {
+        n1 = a.w.n[(size_t)tb * kMaxArms + key1];
+        rb1 = a.w.rbar[(size_t)tb * kMaxArms + key1];
+        eb1 = a.w.ebar[(size_t)tb * kMaxArms + key1];
+    }
+    double S[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) S[e] = a.w.wsorted[(size_t)tb * kWindow + l * E + e];
+    uint32_t wcount = a.w.wmeta[(size_t)tb * 2], whead = a.w.wmeta[(size_t)tb * 2 + 1];
+    const uint32_t M = a.median_window;
+    double *ring = a.w.wring + (size_t)tb * kWindow;
+    double *bg = a.w.b + (size_t)tb * D * kMaxArms;
+    int nact = spopc<G>(act0, sg) + spopc<G>(act1, sg);
+    const StepRec *rp = a.records + (size_t)prm.trace_id * a.rec_stride + a.rec_off;
+    const bool rec_on = prm.record_slot != AGFT_NO_RECORD;
+    const double inv_tau = 1.0 / a.tau;
+    __syncwarp();
+
+    for (uint32_t s = 0; s < a.n_steps; ++s) {
+        const uint32_t t = a.t0 + s;
+        const StepRec *rc = rp + s;
+        double x[D];
+#pragma unroll
+        for (int i = 0; i < D; ++i) x[i] = __ldg(&rc->x[i]);
+        const double alpha = prm.alpha0 * rsqrt(fma((double)t, inv_tau, 1.0));
+
+        // ---- a4: both slots
+        double w[P];
+        {
+            int e = 0;
+#pragma unroll
+            for (int r0 = 0; r0 < D; ++r0)
+#pragma unroll
+                for (int c = r0; c < D; ++c, ++e) w[e] = (r0 == c) ? x[r0] * x[r0] : 2.0 * x[r0] * x[c];
+        }
+        double sc0 = -kInf, mg0 = 0.0, sc1 = -kInf, mg1 = 0.0;
+        if (act0) {
+            double q = 0.0, p = 0.0;
+#pragma unroll
+            for (int e = 0; e < P; ++e) q = fma(w[e], A0[e * 32], q);
+#pragma unroll
+            for (int i = 0; i < D; ++i) p = fma(th0[i], x[i], p);
+            const double bonus = alpha * sqrt(fmax(q, 0.0));
+            sc0 = p + bonus;
+            mg0 = fabs(p) + bonus;
+        }
+        if (act1) {
+            double q = 0.0, p = 0.0;
+#pragma unroll
+            for (int e = 0; e < P; ++e) q = fma(w[e], A1[e * 32], q);
+#pragma unroll
+            for (int i = 0; i < D; ++i) p = fma(th1[i], x[i], p);
+            const double bonus = alpha * sqrt(fmax(q, 0.0));
+            sc1 = p + bonus;
+            mg1 = fabs(p) + bonus;
+        }
+        // ---- a5/a6: lane best (slot 0 keys < slot 1 keys), then segment argmax
+        const bool pick1 = sc1 > sc0;
+        double bs = pick1 ? sc1 : sc0;
+        int bk = act0 || act1 ? (((pick1 ? key1 : key0) << 6) | (pick1 ? 32 : 0) | lane) : 0x7fffffff;
+#pragma unroll
+        for (int off = G / 2; off > 0; off >>= 1) {
+            const double os = __shfl_xor_sync(kFull, bs, off, G);
+            const int ok = __shfl_xor_sync(kFull, bk, off, G);
+            if (os > bs || (os == bs && ok < bk)) { bs = os; bk = ok; }
+        }
+        const int kstar = (bk >> 6) & 127;
+        const int own = (bk & 31) % G;
+        const int oslot = (bk >> 5) & 1;
+        const bool is_own = (l == own);
+        const double mstar = __shfl_sync(kFull, oslot ? mg1 : mg0, own, G);
+        const bool fstar = __shfl_sync(kFull, (int)((oslot ? n1 : n0) == 0u), own, G) != 0;
+        const bool own0 = is_own && oslot == 0, own1 = is_own && oslot == 1;
+        const bool tie = (act0 && !own0 && (bs - sc0 < a.tie_rel * fmax(mstar, mg0)) && !(fstar && n0 == 0u)) ||
+                         (act1 && !own1 && (bs - sc1 < a.tie_rel * fmax(mstar, mg1)) && !(fstar && n1 == 0u));
+        const bool near = sbits<G>(tie, sg) != 0u;
+        const int nact0 = nact;
+        double gapv = kInf;
+        if (a.gap && __any_sync(kFull, rec_on && live)) {
+            double s2 = fmax(act0 && !own0 ? sc0 : -kInf, act1 && !own1 ? sc1 : -kInf);
+            double m2 = (act0 && !own0 && sc0 == s2) ? mg0 : mg1;
+#pragma unroll
+            for (int off = G / 2; off > 0; off >>= 1) {
+                const double os = __shfl_xor_sync(kFull, s2, off, G);
+                const double om = __shfl_xor_sync(kFull, m2, off, G);
+                if (os > s2) { s2 = os; m2 = om; }
+            }
+            const double den = fmax(mstar, m2);
+            gapv = (s2 == -kInf) ? kInf : (den > 0.0 ? (bs - s2) / den : 0.0);
+        }
+
+        // ---- a7: response
+        const Response o = env_response(s_dec[kstar], s_pre[kstar], s_pw[kstar], __ldg(&rc->I), __ldg(&rc->P),
+                                        __ldg(&rc->g), __ldg(&rc->invIm), __ldg(&rc->invAm), __ldg(&rc->wIm),
+                                        __ldg(&rc->nT), __ldg(&rc->nE), invW, q_over, a.u_max, a.u_floor,
+                                        a.p_idle, a.W);
+        // ---- a8: reward + segment window
+        double r = 0.0;
+        if (wcount > 0) {
+            double ref;
+            if (wcount & 1u) {
+                ref = wat<G, E>(S, wcount >> 1);
+            } else {
+                const double m0 = wat<G, E>(S, (wcount >> 1) - 1), m1 = wat<G, E>(S, wcount >> 1);
+                ref = xmul(xadd(m0, m1), 0.5);
+            }
+            r = reward_of(o.edp, ref, a.clip_lo, a.clip_hi);
+        }
+        if (!isfinite(o.edp) || !isfinite(r)) {
+            if (live && l == 0) st.flags |= 1u;
+            live = false;
+        }
+        if (wcount < M) {
+            winsert<G, E>(S, o.edp, wless<G, E>(S, o.edp), l);
+            if (live && l == 0) ring[wcount] = o.edp;
+            ++wcount;
+        } else {
+            const double old = ring[whead];
+            wremove<G, E>(S, wless<G, E>(S, old), l);
+            winsert<G, E>(S, o.edp, wless<G, E>(S, o.edp), l);
+            if (live && l == 0) ring[whead] = o.edp;
+            whead = (whead + 1 == M) ? 0u : whead + 1;
+        }
+
+        // ---- a9: Sherman–Morrison on the owner lane's slot
+        if (live && is_own) {
+            double thv[D];
+#pragma unroll
+            for (int i = 0; i < D; ++i) thv[i] = oslot ? th1[i] : th0[i];
+            sm_update_smem<D>(oslot ? A1 : A0, 32, thv, bg + kstar, kMaxArms, x, r);
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+                if (oslot) th1[i] = thv[i]; else th0[i] = thv[i];
+            }
+            if (oslot) welford(n1, rb1, eb1, r, o.edp);
+            else welford(n0, rb0, eb0, r, o.edp);
+        }
+
+        // ---- a10: pruning (ENV.md §4.8)
+        if (a.prune_enable) {
+            const bool eon = t < a.ext_L;
+            const bool ext0 = act0 && eon && n0 >= a.ext_n && rb0 < prm.extreme_reward_threshold;
+            const bool ext1 = act1 && eon && n1 >= a.ext_n && rb1 < prm.extreme_reward_threshold;
+            const bool q0 = act0 && n0 >= a.hist_n, q1 = act1 && n1 >= a.hist_n;
+            const int next = spopc<G>(ext0, sg) + spopc<G>(ext1, sg);
+            const int nq = spopc<G>(q0, sg) + spopc<G>(q1, sg);
+            const bool need = live && t >= a.hist_t && nq >= 2;
+            bool hist0 = false, hist1 = false;
+            if (__any_sync(kFull, need)) {
+                double best = fmin(q0 ? eb0 : kInf, q1 ? eb1 : kInf);
+#pragma unroll
+                for (int off = G / 2; off > 0; off >>= 1) best = fmin(best, __shfl_xor_sync(kFull, best, off, G));
+                const double dq = (double)(nq > 0 ? nq : 1);
+                const double mu = xdiv(stree<G>(tree, l, q0, key0, eb0, q1, key1, eb1), dq);
+                const double d0 = xsub(eb0, mu), d1 = xsub(eb1, mu);
+                const double sd = xsqrt(xdiv(stree<G>(tree, l, q0, key0, xmul(d0, d0), q1, key1, xmul(d1, d1)), dq));
+                const double thr = xadd(best, xmul(prm.historical_k, sd));
+                hist0 = need && q0 && eb0 > thr;
+                hist1 = need && q1 && eb1 > thr;
+            }
+            const int nh = spopc<G>(hist0, sg) + spopc<G>(hist1, sg);
+            const bool any_rm = live && (next + nh) > 0;
+            if (__any_sync(kFull, any_rm)) {
+                int kc = -1;
+                if ((ext0 || hist0) && (double)(a.f_min_mhz + (uint32_t)key0 * a.f_step_mhz) < a.cascade_limit) kc = key0;
+                if ((ext1 || hist1) && (double)(a.f_min_mhz + (uint32_t)key1 * a.f_step_mhz) < a.cascade_limit) kc = max(kc, key1);
+#pragma unroll
+                for (int off = G / 2; off > 0; off >>= 1) kc = max(kc, __shfl_xor_sync(kFull, kc, off, G));
+                const bool cas0 = act0 && !ext0 && !hist0 && key0 < kc;
+                const bool cas1 = act1 && !ext1 && !hist1 && key1 < kc;
+                const bool c0 = ext0 || hist0 || cas0, c1 = ext1 || hist1 || cas1;
+                const int remaining = spopc<G>(act0 && !c0, sg) + spopc<G>(act1 && !c1, sg);
+                double br = -kInf;
+                int bkr = 0x7fffffff;
+                if (c0) { br = rb0; bkr = key0; }
+                if (c1 && rb1 > br) { br = rb1; bkr = key1; }
+#pragma unroll
+                for (int off = G / 2; off > 0; off >>= 1) {
+                    const double ob = __shfl_xor_sync(kFull, br, off, G);
+                    const int ok = __shfl_xor_sync(kFull, bkr, off, G);
+                    if (ob > br || (ob == br && ok < bkr)) { br = ob; bkr = ok; }
+                }
+                const int restore = remaining == 0 ? bkr : -1;       // AMB-11
+                const bool rm0 = any_rm && c0 && key0 != restore, rm1 = any_rm && c1 && key1 != restore;
+                const int ce = spopc<G>(rm0 && ext0, sg) + spopc<G>(rm1 && ext1, sg);
+                const int ch = spopc<G>(rm0 && !ext0 && hist0, sg) + spopc<G>(rm1 && !ext1 && hist1, sg);
+                const int cc = spopc<G>(rm0 && !ext0 && !hist0, sg) + spopc<G>(rm1 && !ext1 && !hist1, sg);
+                if (any_rm) {
+                    if (l == 0) {
+                        st.n_pruned_extreme += ce;
+                        st.n_pruned_hist += ch;
+                        st.n_pruned_cascade += cc;
+                    }
+                    nact -= ce + ch + cc;
+                }
+                if (rm0) act0 = false;
+                if (rm1) act1 = false;
+            }
+        }
+
+        // ---- a11
+        if (live && l == 0) {
+            stats_add(st, o, r, __ldg(&rc->baseE), __ldg(&rc->baseEDP), kstar, (uint32_t)nact0);
+            st.near_tie_steps += near ? 1u : 0u;
+            if (rec_on) {
+                if (a.traj) a.traj[(size_t)prm.record_slot * a.rec_stride + a.rec_off + s] = (uint8_t)kstar;
+                if (a.gap) a.gap[(size_t)prm.record_slot * a.rec_stride + a.rec_off + s] = gapv;
+            }
+            if (a.chosen) a.chosen[tb] = (uint32_t)kstar;
+        }
+    }
+
+    // ---- write back (segments of real tuners only)
+    __syncwarp();
+    if (valid) {
+        if (has0) {
+#pragma unroll
+            for (int e = 0; e < P; ++e) a.w.ainv[((size_t)tb * P + e) * kMaxArms + key0] = A0[e * 32];
+#pragma unroll
+            for (int r = 0; r < D; ++r) a.w.theta[((size_t)tb * D + r) * kMaxArms + key0] = th0[r];
+            a.w.n[(size_t)tb * kMaxArms + key0] = n0;
+            a.w.rbar[(size_t)tb * kMaxArms + key0] = rb0;
+            a.w.ebar[(size_t)tb * kMaxArms + key0] = eb0;
+        }
+        if (has1) {
+#pragma unroll
+            for (int e = 0; e < P; ++e) a.w.ainv[((size_t)tb * P + e) * kMaxArms + key1] = A1[e * 32];
+#pragma unroll
+            for (int r = 0; r < D; ++r) a.w.theta[((size_t)tb * D + r) * kMaxArms + key1] = th1[r];
+            a.w.n[(size_t)tb * kMaxArms + key1] = n1;
+            a.w.rbar[(size_t)tb * kMaxArms + key1] = rb1;
+            a.w.ebar[(size_t)tb * kMaxArms + key1] = eb1;
+        }
+#pragma unroll
+        for (int e = 0; e < E; ++e) a.w.wsorted[(size_t)tb * kWindow + l * E + e] = S[e];
+    }
+    uint32_t words[4];
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+        uint32_t bits = ((act0 && (key0 >> 5) == w) ? (1u << (key0 & 31)) : 0u) |
+                        ((act1 && (key1 >> 5) == w) ? (1u << (key1 & 31)) : 0u);
+#pragma unroll
+        for (int off = G / 2; off > 0; off >>= 1) bits |= __shfl_xor_sync(kFull, bits, off, G);
+        words[w] = bits;
+    }
+    if (valid && l == 0) {
+        *reinterpret_cast<uint4 *>(a.w.active + (size_t)tb * 4) = make_uint4(words[0], words[1], words[2], words[3]);
+        a.w.wmeta[(size_t)tb * 2] = wcount;
+        a.w.wmeta[(size_t)tb * 2 + 1] = whead;
+        st.n_active = (uint32_t)nact;
+        a.w.acc[tb] = st;
+    }
+}
+
+template <int D, int G>
+static cudaError_t launch_seg2_dg(const ReplayArgs &a, cudaStream_t s)
+{
+    constexpr int P = D * (D + 1) / 2;
+    constexpr int per_block = kSeg2Warps * (32 / G);
+    const size_t smem = seg2_smem_bytes<G>(P);
+    auto kern = seg2_kernel<D, G>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const uint32_t blocks = (a.n_tuners + per_block - 1) / per_block;
+    kern<<<blocks, kSeg2Warps * 32, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+template <int D>
+static cudaError_t launch_seg2_d(const ReplayArgs &a, int G, cudaStream_t s)
+{
+    switch (G) {
+    case 4: return launch_seg2_dg<D, 4>(a, s);
+    case 8: return launch_seg2_dg<D, 8>(a, s);
+    default: return launch_seg2_dg<D, 16>(a, s);
+    }
+}
+
+// K_act ≤ 2G
+cudaError_t launch_seg2(const ReplayArgs &a, uint32_t D, int G, cudaStream_t s)
+{
+    if (a.n_tuners == 0 || a.n_steps == 0) return cudaSuccess;
+    switch (D) {
+    case 1: return launch_seg2_d<1>(a, G, s);
+    case 2: return launch_seg2_d<2>(a, G, s);
+    case 3: return launch_seg2_d<3>(a, G, s);
+    case 4: return launch_seg2_d<4>(a, G, s);
+    case 5: return launch_seg2_d<5>(a, G, s);
+    case 6: return launch_seg2_d<6>(a, G, s);
+    default: return launch_seg2_d<7>(a, G, s);
+    }
+}
+
+}  // namespace agft

@@ -15,10 +15,14 @@ namespace agft {
 
 namespace {
 constexpr int kSoloThreads = 64;
+#ifndef AGFT_SOLO_MIN_BLOCKS
+#define AGFT_SOLO_MIN_BLOCKS 4          // as SEG2: an occupancy cap (≤ 168 regs) spilled and measured slower
+#endif
+constexpr int kSoloMinBlocks = AGFT_SOLO_MIN_BLOCKS;
 }
 
 template <int D>
-__global__ void __launch_bounds__(kSoloThreads) solo_kernel(const __grid_constant__ ReplayArgs a)
+__global__ void __launch_bounds__(kSoloThreads, kSoloMinBlocks) solo_kernel(const __grid_constant__ ReplayArgs a)
 {
     constexpr int P = D * (D + 1) / 2;
     __shared__ double S_[kWindow * kSoloThreads];
@@ -56,64 +60,32 @@ __global__ void __launch_bounds__(kSoloThreads) solo_kernel(const __grid_constan
     const StepRec *rp = a.records + (size_t)prm.trace_id * a.rec_stride + a.rec_off;
     const bool rec_on = prm.record_slot != AGFT_NO_RECORD;
 
-    double x[D];
-    RecView v;
-    load_rec<D>(rp, x, v);
+    const SmemWindow win{S, kSoloThreads};
+    double oldest = ring_oldest(ring, wcount, whead, M);
     for (uint32_t s = 0; s < a.n_steps; ++s) {
-        double xn[D];
-        RecView vn;
-        if (s + 1 < a.n_steps) load_rec<D>(rp + s + 1, xn, vn);   // prefetch the next window
-
+        const StepRec *rc = rp + s;                       // shared by the lanes of a trace: L1 broadcast
         // a7: response at the only active frequency
-        const Response o = env_response(dec, pre, pw, v.I, v.P, v.g, v.invIm, v.invAm, v.wIm, v.nT, v.nE,
-                                        invW, q_over, a.u_max, a.u_floor, a.p_idle, a.W);
+        const Response o = env_response(dec, pre, pw, __ldg(&rc->I), __ldg(&rc->P), __ldg(&rc->g),
+                                        __ldg(&rc->invIm), __ldg(&rc->invAm), __ldg(&rc->wIm), __ldg(&rc->nT),
+                                        __ldg(&rc->nE), invW, q_over, a.u_max, a.u_floor, a.p_idle, a.W);
         // a8: reward against the median of the window, then push the EDP
-        double r = 0.0;
-        if (wcount > 0) {
-            const double ref = (wcount & 1u) ? SW(wcount >> 1)
-                                             : xmul(xadd(SW((wcount >> 1) - 1), SW(wcount >> 1)), 0.5);
-            r = reward_of(o.edp, ref, a.clip_lo, a.clip_hi);
-        }
-        if (!isfinite(o.edp) || !isfinite(r)) {
+        bool ok;
+        const double r = reward_and_push(win, ring, wcount, whead, M, o.edp, a.clip_lo, a.clip_hi, ok, oldest);
+        if (!ok) {
             st.flags |= 1u;
             break;
         }
-        if (wcount < M) {
-            int j = (int)wcount;
-            while (j > 0 && SW(j - 1) > o.edp) { SW(j) = SW(j - 1); --j; }
-            SW(j) = o.edp;
-            ring[wcount] = o.edp;
-            ++wcount;
-        } else {
-            const double old = ring[whead];
-            int lo = 0, hi = (int)M;                       // lower_bound(old): S[lo] == old
-            while (lo < hi) {
-                const int mid = (lo + hi) >> 1;
-                if (SW(mid) < old) lo = mid + 1; else hi = mid;
-            }
-            int j = lo;
-            if (o.edp < old) {
-                while (j > 0 && SW(j - 1) > o.edp) { SW(j) = SW(j - 1); --j; }
-            } else {
-                while (j < (int)M - 1 && SW(j + 1) < o.edp) { SW(j) = SW(j + 1); ++j; }
-            }
-            SW(j) = o.edp;
-            ring[whead] = o.edp;
-            whead = (whead + 1 == M) ? 0u : whead + 1;
-        }
         // a9: Eqs. 3–5 on the (only) chosen arm, Welford means
+        double x[D];
+#pragma unroll
+        for (int q = 0; q < D; ++q) x[q] = __ldg(&rc->x[q]);
         sm_update<D>(A, th, b, x, r);
         welford(n, rbar, ebar, r, o.edp);
         // a11
-        stats_add(st, o, r, v.baseE, v.baseEDP, k, 1u);
+        stats_add(st, o, r, __ldg(&rc->baseE), __ldg(&rc->baseEDP), k, 1u);
         if (rec_on) {
             if (a.traj) a.traj[(size_t)prm.record_slot * a.rec_stride + a.rec_off + s] = (uint8_t)k;
             if (a.gap) a.gap[(size_t)prm.record_slot * a.rec_stride + a.rec_off + s] = kInf;
-        }
-        if (s + 1 < a.n_steps) {
-#pragma unroll
-            for (int q = 0; q < D; ++q) x[q] = xn[q];
-            v = vn;
         }
     }
     if (a.chosen) a.chosen[tb] = (uint32_t)k;

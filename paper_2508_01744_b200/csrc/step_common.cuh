@@ -119,36 +119,46 @@ struct SmemWindow {
     {
         return (n & 1u) ? at(n >> 1) : xmul(xadd(at((n >> 1) - 1), at(n >> 1)), 0.5);
     }
-    // insert into a window holding n < M values
+    // #(S[0..n) < v): branch-free binary search (n ≤ 64)
+    __device__ __forceinline__ int count_less(int n, double v) const
+    {
+        int lo = 0;
+#pragma unroll
+        for (int step = 64; step > 0; step >>= 1)
+            if (lo + step <= n && at(lo + step - 1) < v) lo += step;
+        return lo;
+    }
+    // insert into a window holding n < M values: position by binary search, then a
+    // fixed-length shift whose loads are independent (pipelined, no data-dependent exit)
     __device__ __forceinline__ void insert(uint32_t n, double v) const
     {
-        int j = (int)n;
-        while (j > 0 && at(j - 1) > v) { at(j) = at(j - 1); --j; }
-        at(j) = v;
+        const int p = count_less((int)n, v);
+        for (int j = (int)n; j > p; --j) at(j) = at(j - 1);
+        at(p) = v;
     }
-    // replace `old` (present) by v in a full window of M values: binary search, then an
-    // insertion-sort walk from the evicted slot toward v's position
+    // replace `old` (present) by v in a full window of M values: both positions by binary
+    // search (independent), then shift the elements between them by one slot
     __device__ __forceinline__ void replace(uint32_t M, double old, double v) const
     {
-        int lo = 0, hi = (int)M;
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (at(mid) < old) lo = mid + 1; else hi = mid;
-        }
-        int j = lo;
-        if (v < old) {
-            while (j > 0 && at(j - 1) > v) { at(j) = at(j - 1); --j; }
-        } else {
-            while (j < (int)M - 1 && at(j + 1) < v) { at(j) = at(j + 1); ++j; }
-        }
-        at(j) = v;
+        const int po = count_less((int)M, old);            // S[po] == old
+        const int lv = count_less((int)M, v);               // #(S < v), old included
+        if (v < old) {                                      // v lands at lv ≤ po: shift [lv, po) up
+            for (int j = po; j > lv; --j) at(j) = at(j - 1);
+            at(lv) = v;
+        } else if (v > old) {                               // v lands at lv − 1 ≥ po: shift (po, lv) down
+            const int pn = lv - 1;
+            for (int j = po; j < pn; ++j) at(j) = at(j + 1);
+            at(pn) = v;
+        }                                                   // v == old: the multiset is unchanged
     }
 };
 
-// a8 for a lane-private window: reward against the median of the window, then push edp
+// a8 for a lane-private window: reward against the median of the window, then push edp.
+// `oldest` carries the ring value that the next push evicts (ring[whead] of a full window),
+// loaded one step ahead so its global-memory latency overlaps the step.
 __device__ __forceinline__ double reward_and_push(const SmemWindow &win, double *ring, uint32_t &wcount,
                                                   uint32_t &whead, uint32_t M, double edp, double clip_lo,
-                                                  double clip_hi, bool &finite_ok)
+                                                  double clip_hi, bool &finite_ok, double &oldest)
 {
     double r = 0.0;
     if (wcount > 0) r = reward_of(edp, win.median(wcount), clip_lo, clip_hi);
@@ -159,12 +169,56 @@ __device__ __forceinline__ double reward_and_push(const SmemWindow &win, double 
         ring[wcount] = edp;
         ++wcount;
     } else {
-        const double old = ring[whead];
-        win.replace(M, old, edp);
+        win.replace(M, oldest, edp);
         ring[whead] = edp;
         whead = (whead + 1 == M) ? 0u : whead + 1;
     }
+    if (wcount == M) oldest = ring[whead];
     return r;
+}
+
+__device__ __forceinline__ double ring_oldest(const double *ring, uint32_t wcount, uint32_t whead, uint32_t M)
+{
+    return wcount == M ? ring[whead] : 0.0;
+}
+
+// The same update with the packed A⁻¹ held in shared memory (entry e at Ac[e * stride]),
+// updated in place — keeps only z in registers.
+template <int D>
+__device__ __forceinline__ void sm_update_smem(double *Ac, int stride, double (&th)[D], double *bcol,
+                                               int bstride, const double (&x)[D], double r)
+{
+    double z[D];
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        double acc = 0.0;
+#pragma unroll
+        for (int c = 0; c < D; ++c) acc = fma(Ac[(i <= c ? pidx<D>(i, c) : pidx<D>(c, i)) * stride], x[c], acc);
+        z[i] = acc;
+    }
+    double xz = 0.0, px = 0.0;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        xz = fma(x[i], z[i], xz);
+        px = fma(th[i], x[i], px);
+    }
+    const double invd = 1.0 / (1.0 + xz);
+#pragma unroll
+    for (int r0 = 0; r0 < D; ++r0) {
+        const double zr = -z[r0] * invd;
+#pragma unroll
+        for (int c = r0; c < D; ++c) {
+            double &ae = Ac[pidx<D>(r0, c) * stride];
+            ae = fma(zr, z[c], ae);
+        }
+    }
+    const double coef = (r - px) * invd;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        th[i] = fma(z[i], coef, th[i]);
+        double &bi = bcol[(size_t)i * bstride];
+        bi = xadd(bi, xmul(r, x[i]));
+    }
 }
 
 // one record's fields, loaded once per step

@@ -287,6 +287,7 @@ static agft_status run_steps(agft_handle h, const void *d_records, uint32_t t0, 
                 case kClsSeg32: e = split ? launch_seg2(ak, c.d, 16, h->side[k]) : launch_mseg(ak, c.d, mseg_g(), h->side[k]); break;
                 case kClsSeg16: e = launch_seg2(ak, c.d, 8, h->side[k]); break;
                 case kClsSeg8: e = launch_seg2(ak, c.d, 4, h->side[k]); break;
+                case kClsSeg64: e = launch_seg2(ak, c.d, 32, h->side[k]); break;
                 default: e = launch_solo(ak, c.d, h->side[k]); break;
                 }
                 if (e == cudaSuccess) e = cudaEventRecord(h->join[k], h->side[k]);

@@ -13,13 +13,11 @@
 // The canonical 128-slot reduction of ENV.md §4.8 maps onto this layout exactly:
 // levels 1–5 are the xor-butterfly across lanes (adjacent arms are adjacent lanes),
 // levels 6–7 combine the four slot partials in-lane.
-#include "agft_internal.cuh"
+#include "step_common.cuh"
 
 namespace agft {
 
 namespace {
-
-constexpr double kInf = __builtin_huge_val();
 
 template <int S, typename T>
 __device__ __forceinline__ T pick(const T (&v)[S], int j)
@@ -156,7 +154,7 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
         for (int j = 0; j < S; ++j) nact += popc_ballot((act >> j) & 1u);
 
         // ---- a3: α_t = α0/√(1+t/τ)
-        const double alpha = prm.alpha0 / sqrt(1.0 + (double)t / a.tau);
+        const double alpha = alpha_t(prm.alpha0, t, 1.0 / a.tau);
 
         // ---- a4: Eq. 1 scores.  q = Σ_{i≤j} w_ij A⁻¹_ij with w_ij = x_i x_j (×2 off-diagonal)
         double w[P];
@@ -178,9 +176,8 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
             if ((act >> j) & 1u) {
                 const double *Aj = sA + j * P * 32 + lane;
                 const double *Tj = sT + j * D * 32 + lane;
-                double q = 0.0, p = 0.0;
-#pragma unroll
-                for (int e = 0; e < P; ++e) q = fma(w[e], Aj[e * 32], q);
+                const double q = quad_form<P>(w, Aj, 32);
+                double p = 0.0;
 #pragma unroll
                 for (int i = 0; i < D; ++i) p = fma(Tj[i * 32], x[i], p);
                 const double bonus = alpha * sqrt(fmax(q, 0.0));   // AMB-19

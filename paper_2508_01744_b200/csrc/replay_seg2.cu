@@ -84,18 +84,25 @@ __device__ __forceinline__ void winsert(double (&S)[E], double v, int pi, int l)
     }
 }
 
-// canonical tree: scatter (has0,key0,v0), (has1,key1,v1) of every lane to `buf` (128 zeros
-// on entry, restored to zeros on exit), reduce aligned blocks, butterfly
+// per-segment tree buffer: slot k at k + k/SL (one pad per 128/G-slot block, odd stride) so
+// that the lanes' block reads fall in different banks
+template <int G>
+__host__ __device__ constexpr int tree_stride() { return 128 + G + 1; }
+template <int G>
+__device__ __forceinline__ int tslot(int k) { return k + k / (128 / G); }
+
+// canonical tree: scatter (has0,key0,v0), (has1,key1,v1) of every lane to `buf` (zeros on
+// entry, restored to zeros on exit), reduce aligned blocks pairwise, butterfly
 template <int G>
 __device__ __forceinline__ double stree(double *buf, int l, bool h0, int k0, double v0, bool h1, int k1, double v1)
 {
     constexpr int SL = 128 / G;
-    if (h0) buf[k0] = v0;
-    if (h1) buf[k1] = v1;
+    if (h0) buf[tslot<G>(k0)] = v0;
+    if (h1) buf[tslot<G>(k1)] = v1;
     __syncwarp();
     double v[SL];
 #pragma unroll
-    for (int j = 0; j < SL; ++j) v[j] = buf[l * SL + j];
+    for (int j = 0; j < SL; ++j) v[j] = buf[l * (SL + 1) + j];
 #pragma unroll
     for (int len = SL; len > 1; len >>= 1)
 #pragma unroll
@@ -104,8 +111,8 @@ __device__ __forceinline__ double stree(double *buf, int l, bool h0, int k0, dou
 #pragma unroll
     for (int off = 1; off < G; off <<= 1) s = xadd(s, __shfl_xor_sync(kFull, s, off, G));
     __syncwarp();
-    if (h0) buf[k0] = 0.0;
-    if (h1) buf[k1] = 0.0;
+    if (h0) buf[tslot<G>(k0)] = 0.0;
+    if (h1) buf[tslot<G>(k1)] = 0.0;
     __syncwarp();
     return s;
 }
@@ -113,7 +120,7 @@ __device__ __forceinline__ double stree(double *buf, int l, bool h0, int k0, dou
 template <int G>
 constexpr size_t seg2_smem_bytes(int P)
 {
-    return (3 * kMaxArms + (size_t)kSeg2Warps * 2 * P * 32 + (size_t)kSeg2Warps * (32 / G) * kMaxArms) * 8 +
+    return (3 * kMaxArms + (size_t)kSeg2Warps * 2 * P * 32 + (size_t)kSeg2Warps * (32 / G) * tree_stride<G>()) * 8 +
            (size_t)kSeg2Warps * (32 / G) * sizeof(agft_tuner_stats);
 }
 
@@ -128,15 +135,15 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
     extern __shared__ double sm[];
     double *s_dec = sm, *s_pre = sm + kMaxArms, *s_pw = sm + 2 * kMaxArms;
     double *s_A = sm + 3 * kMaxArms;                                   // [warp][slot][P][32]
-    double *s_tree = s_A + kSeg2Warps * 2 * P * 32;                    // [warp][seg][128]
-    agft_tuner_stats *s_st = reinterpret_cast<agft_tuner_stats *>(s_tree + kSeg2Warps * NSEG * kMaxArms);
+    double *s_tree = s_A + kSeg2Warps * 2 * P * 32;                    // [warp][seg][tree_stride]
+    agft_tuner_stats *s_st = reinterpret_cast<agft_tuner_stats *>(s_tree + kSeg2Warps * NSEG * tree_stride<G>());
     const EnvConsts *ec = a.w.env;
     for (int q = threadIdx.x; q < kMaxArms; q += blockDim.x) {
         s_dec[q] = ec->dec[q];
         s_pre[q] = ec->pre[q];
         s_pw[q] = ec->pw[q];
     }
-    for (int q = threadIdx.x; q < kSeg2Warps * NSEG * kMaxArms; q += blockDim.x) s_tree[q] = 0.0;
+    for (int q = threadIdx.x; q < kSeg2Warps * NSEG * tree_stride<G>(); q += blockDim.x) s_tree[q] = 0.0;
     __syncthreads();
     const double invW = ec->invW, q_over = ec->q_over;
 
@@ -148,7 +155,7 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
     const uint32_t idx = wbase + sg;
     const bool valid = idx < cnt;
     const uint32_t tb = a.list ? a.list[valid ? idx : cnt - 1] : (valid ? idx : cnt - 1);
-    double *tree = s_tree + (warp * NSEG + sg) * kMaxArms;
+    double *tree = s_tree + (warp * NSEG + sg) * tree_stride<G>();
     double *A0 = s_A + (warp * 2 + 0) * P * 32 + lane;                 // slot 0 column
     double *A1 = s_A + (warp * 2 + 1) * P * 32 + lane;                 // slot 1 column
     agft_tuner_stats &st = s_st[warp * NSEG + sg];
@@ -219,22 +226,15 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
         double x[D];
 #pragma unroll
         for (int i = 0; i < D; ++i) x[i] = __ldg(&rc->x[i]);
-        const double alpha = prm.alpha0 * rsqrt(fma((double)t, inv_tau, 1.0));
+        const double alpha = alpha_t(prm.alpha0, t, inv_tau);
 
         // ---- a4: both slots
         double w[P];
-        {
-            int e = 0;
-#pragma unroll
-            for (int r0 = 0; r0 < D; ++r0)
-#pragma unroll
-                for (int c = r0; c < D; ++c, ++e) w[e] = (r0 == c) ? x[r0] * x[r0] : 2.0 * x[r0] * x[c];
-        }
+        pair_weights<D>(x, w);
         double sc0 = -kInf, mg0 = 0.0, sc1 = -kInf, mg1 = 0.0;
         if (act0) {
-            double q = 0.0, p = 0.0;
-#pragma unroll
-            for (int e = 0; e < P; ++e) q = fma(w[e], A0[e * 32], q);
+            const double q = quad_form<P>(w, A0, 32);
+            double p = 0.0;
 #pragma unroll
             for (int i = 0; i < D; ++i) p = fma(th0[i], x[i], p);
             const double bonus = alpha * sqrt(fmax(q, 0.0));
@@ -242,9 +242,8 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
             mg0 = fabs(p) + bonus;
         }
         if (act1) {
-            double q = 0.0, p = 0.0;
-#pragma unroll
-            for (int e = 0; e < P; ++e) q = fma(w[e], A1[e * 32], q);
+            const double q = quad_form<P>(w, A1, 32);
+            double p = 0.0;
 #pragma unroll
             for (int i = 0; i < D; ++i) p = fma(th1[i], x[i], p);
             const double bonus = alpha * sqrt(fmax(q, 0.0));
@@ -468,6 +467,7 @@ static cudaError_t launch_seg2_d(const ReplayArgs &a, int G, cudaStream_t s)
 {
     switch (G) {
     case 4: return launch_seg2_dg<D, 4>(a, s);
+    case 32: return launch_seg2_dg<D, 32>(a, s);
     case 8: return launch_seg2_dg<D, 8>(a, s);
     default: return launch_seg2_dg<D, 16>(a, s);
     }

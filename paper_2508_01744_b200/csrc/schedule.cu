@@ -22,6 +22,7 @@ __device__ __forceinline__ int class_of(const Ws &w, uint32_t tb, bool split)
     if (k <= 8) return kClsSeg8;
     if (k <= 16) return kClsSeg16;
     if (k <= 32) return kClsSeg32;
+    if (split && k <= 64) return kClsSeg64;
     return kClsWide;
 }
 

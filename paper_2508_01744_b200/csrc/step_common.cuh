@@ -66,6 +66,39 @@ __device__ __forceinline__ void stats_add(agft_tuner_stats &st, const Response &
     st.last_arm = (uint32_t)kstar;
 }
 
+// Eq. 1's quadratic form xᵀA⁻¹x = Σ_e w_e·A⁻¹_e over the packed upper triangle (w_e = x_i x_j,
+// doubled off the diagonal), in four independent FMA chains (ILP; scores are
+// tolerance-compared, ENV.md §4.3)
+template <int P>
+__device__ __forceinline__ double quad_form(const double (&w)[P], const double *A, int stride)
+{
+    double q0 = 0.0, q1 = 0.0, q2 = 0.0, q3 = 0.0;
+#pragma unroll
+    for (int e = 0; e < P; e += 4) {
+        q0 = fma(w[e], A[e * stride], q0);
+        if (e + 1 < P) q1 = fma(w[e + 1 < P ? e + 1 : e], A[(e + 1 < P ? e + 1 : e) * stride], q1);
+        if (e + 2 < P) q2 = fma(w[e + 2 < P ? e + 2 : e], A[(e + 2 < P ? e + 2 : e) * stride], q2);
+        if (e + 3 < P) q3 = fma(w[e + 3 < P ? e + 3 : e], A[(e + 3 < P ? e + 3 : e) * stride], q3);
+    }
+    return (q0 + q1) + (q2 + q3);
+}
+
+template <int D>
+__device__ __forceinline__ void pair_weights(const double (&x)[D], double (&w)[D * (D + 1) / 2])
+{
+    int e = 0;
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+#pragma unroll
+        for (int c = r; c < D; ++c, ++e) w[e] = (r == c) ? x[r] * x[r] : 2.0 * x[r] * x[c];
+}
+
+// a3: α_t = α0/√(1 + t/τ) (AMB-1), via one reciprocal square root
+__device__ __forceinline__ double alpha_t(double alpha0, uint32_t t, double inv_tau)
+{
+    return alpha0 * rsqrt(fma((double)t, inv_tau, 1.0));
+}
+
 // packed upper-triangle index of (r, c), r ≤ c, for a D×D symmetric matrix
 template <int D>
 __device__ __forceinline__ constexpr int pidx(int r, int c)

@@ -126,6 +126,12 @@ def lib():
                                        C.POINTER(OrcStats), C.POINTER(OrcArms), C.POINTER(OrcRecord)]
         L.orc_reward.argtypes = [f64, C.POINTER(f64), u32, f64, f64]
         L.orc_reward.restype = f64
+        L.orc_prototype.argtypes = [C.POINTER(OrcConfig), u32, u32]
+        L.orc_prototype.restype = u32
+        L.orc_sweep.argtypes = [C.POINTER(OrcConfig), u32, u32, u32, C.POINTER(f64), C.POINTER(f64),
+                                C.POINTER(u32), C.POINTER(f64), C.POINTER(C.c_uint8)]
+        L.orc_argmin.argtypes = [C.POINTER(f64), u32, u32]
+        L.orc_argmin.restype = u32
         L.orc_sizeof.argtypes = [C.c_int]
         L.orc_sizeof.restype = u32
         for i, s in enumerate([OrcConfig, OrcTuner, OrcStats, OrcArms, OrcStepRec, OrcRecord,
@@ -339,3 +345,30 @@ def run_batch(cfg: dict, params: dict, T: int, threads: int = 0):
     rc = lib().orc_run_batch(C.byref(oc), tuners, n, T, threads, stats)
     assert rc == 0, rc
     return [_stats_dict(stats[i]) for i in range(n)]
+
+
+def prototype(cfg: dict, trace_id: int, t: int) -> int:
+    """ENV.md §2.2: the Table-1 prototype index of window t of trace trace_id."""
+    return int(lib().orc_prototype(C.byref(make_config(cfg)), trace_id, t))
+
+
+def new_sweep(cfg: dict) -> dict:
+    """Zeroed ENV.md §5 accumulators for one trace."""
+    K = cfg["n_arms"]
+    return {"S": np.zeros((K, 3)), "SP": np.zeros((5, K)), "NP": np.zeros(5, np.uint32), "O": np.zeros(2)}
+
+
+def sweep(cfg: dict, trace_id: int, t0: int, n: int, acc: dict | None = None, best: bool = False):
+    """ENV.md §5 over windows [t0, t0+n) of one trace, accumulating into ``acc`` (new if None).
+    Returns (acc, per-window oracle arm k° or None)."""
+    acc = new_sweep(cfg) if acc is None else acc
+    b = np.zeros(n, np.uint8) if best else None
+    lib().orc_sweep(C.byref(make_config(cfg)), trace_id, t0, n, _ptr(acc["S"], f64), _ptr(acc["SP"], f64),
+                    _ptr(acc["NP"], u32), _ptr(acc["O"], f64), _ptr(b, C.c_uint8) if best else None)
+    return acc, b
+
+
+def offline_arm(values) -> int:
+    """Smallest index minimising ``values`` (ENV.md §5 k_off)."""
+    v = np.ascontiguousarray(values, dtype=np.float64)
+    return int(lib().orc_argmin(_ptr(v, f64), len(v), 1))

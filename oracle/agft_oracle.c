@@ -68,6 +68,21 @@ static double u53(uint32_t a, uint32_t b)
 
 static uint32_t umin(uint32_t a, uint32_t b) { return a < b ? a : b; }
 
+/* ENV.md §2.2: the Table-1 prototype of the 10-minute segment holding window t */
+uint32_t orc_prototype(const orc_config *c, uint32_t r, uint32_t t)
+{
+    uint32_t u4[4];
+    draw(c, r, t / c->seg_steps, 1, 0, 0, u4);
+    uint32_t v = u4[0] >> 24;
+    uint32_t p = 0, cum = 0;
+    for (p = 0; p < 5; ++p) {
+        cum += c->weight[p];
+        if (v < cum) break;
+    }
+    if (p >= 5) p = 4;
+    return p;
+}
+
 /* ---------------------------------------------------------------- ENV-T (ENV.md §2.2)
  * Shapes: Table 1 prototypes, §2.4 non-stationarity.
  * parity unpinned (vs paper): the Azure trace is proprietary (AMB-23). */
@@ -79,14 +94,7 @@ void orc_trace_row(const orc_config *c, uint32_t r, uint32_t t, uint32_t row[ORC
     else pattern = 1 + r % 2;
 
     uint32_t u4[4];
-    draw(c, r, t / c->seg_steps, 1, 0, 0, u4);
-    uint32_t v = u4[0] >> 24;
-    uint32_t p = 0, cum = 0;
-    for (p = 0; p < 5; ++p) {
-        cum += c->weight[p];
-        if (v < cum) break;
-    }
-    if (p >= 5) p = 4;
+    uint32_t p = orc_prototype(c, r, t);
 
     double m = 1.0;
     if (pattern >= 1) {
@@ -224,6 +232,52 @@ void orc_env_response(const orc_config *c, const uint32_t row[ORC_ROW_WORDS], ui
     orc_steprec rec;
     orc_step_record(c, row, &rec);
     orc_response(c, &rec, F, out);
+}
+
+/* ---------------------------------------------------------------- offline sweep (ENV.md §5)
+ * every frequency of the grid held fixed over the same windows; Table 6
+ * "Offline" = the EDP-minimising fixed frequency.  Plain loops in the order
+ * §5 writes; sums accumulate (+=) across calls in ascending t. */
+void orc_sweep(const orc_config *c, uint32_t r, uint32_t t0, uint32_t n, double *S /*[K][3]*/,
+               double *SP /*[5][K]*/, uint32_t *NP /*[5]*/, double *O /*[2]*/, uint8_t *best /*[n] or NULL*/)
+{
+    uint32_t K = c->n_arms;
+    for (uint32_t i = 0; i < n; ++i) {
+        uint32_t t = t0 + i;
+        uint32_t row[ORC_ROW_WORDS];
+        orc_trace_row(c, r, t, row);
+        orc_steprec rec;
+        orc_step_record(c, row, &rec);
+        uint32_t p = orc_prototype(c, r, t);
+        NP[p] += 1u;
+        uint32_t kb = 0;
+        double eb = 0.0, Eb = 0.0;
+        for (uint32_t k = 0; k < K; ++k) {
+            double out[4];
+            orc_response(c, &rec, c->f_min_mhz + k * c->f_step_mhz, out);
+            S[3 * k + 0] = S[3 * k + 0] + out[0];
+            S[3 * k + 1] = S[3 * k + 1] + out[1];
+            S[3 * k + 2] = S[3 * k + 2] + out[3];
+            SP[p * K + k] = SP[p * K + k] + out[3];
+            if (k == 0 || out[3] < eb) {          /* strict: ties keep the smaller k */
+                kb = k;
+                eb = out[3];
+                Eb = out[0];
+            }
+        }
+        O[0] = O[0] + eb;
+        O[1] = O[1] + Eb;
+        if (best) best[i] = (uint8_t)kb;
+    }
+}
+
+/* smallest k minimising v[k * stride] over k < K */
+uint32_t orc_argmin(const double *v, uint32_t K, uint32_t stride)
+{
+    uint32_t kb = 0;
+    for (uint32_t k = 1; k < K; ++k)
+        if (v[k * stride] < v[kb * stride]) kb = k;
+    return kb;
 }
 
 /* ---------------------------------------------------------------- small helpers */

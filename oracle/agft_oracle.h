@@ -91,6 +91,7 @@ typedef struct {                       /* unit-test environment: replaces ENV-T/
 #define ORC_FREE 255                   /* follow[t] == ORC_FREE: no forced choice at step t */
 
 void orc_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
+uint32_t orc_prototype(const orc_config *c, uint32_t trace_id, uint32_t t);
 void orc_trace_row(const orc_config *c, uint32_t trace_id, uint32_t t, uint32_t row[ORC_ROW_WORDS]);
 void orc_trace_rows(const orc_config *c, uint32_t trace_id, uint32_t t0, uint32_t n,
                     uint32_t *rows /* [n][12] */);
@@ -116,6 +117,11 @@ int orc_run_tuner_ex(const orc_config *c, const orc_tuner *tu, uint32_t T, const
                      const orc_inject *inj, orc_stats *stats, orc_arms *arms, const orc_record *rec);
 
 /* struct sizes, for the Python mirror's layout check */
+/* ENV.md §5 offline sweep (accumulating) and argmin helper */
+void orc_sweep(const orc_config *c, uint32_t trace_id, uint32_t t0, uint32_t n, double *S /*[K][3]*/,
+               double *SP /*[5][K]*/, uint32_t *NP /*[5]*/, double *O /*[2]*/, uint8_t *best /*[n] or NULL*/);
+uint32_t orc_argmin(const double *v, uint32_t K, uint32_t stride);
+
 uint32_t orc_sizeof(int which /* 0 config 1 tuner 2 stats 3 arms 4 steprec 5 record 6 inject */);
 
 /* Free-running batch over a pthread pool; stats[i] for tuners[i]. threads<=0: all cores. */

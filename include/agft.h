@@ -185,6 +185,30 @@ agft_status agft_run(const agft_config *cfg, const agft_tuner_params *h_params,
                      void *d_workspace, size_t ws_bytes, void *d_scratch, size_t scratch_bytes,
                      agft_tuner_stats *d_stats_buf, agft_tuner_stats *h_stats, void *stream);
 
+/* ---- Offline frequency sweep (ENV.md §5): every arm of the grid
+ * held fixed over the same windows, as the paper's offline sweep does ("we iterated
+ * through all core frequencies … calculated the corresponding EDP"), giving Table 6's
+ * "Offline" optimum and each tuner's regret.
+ *
+ * agft_sweep: windows [t0, t0+n_steps) of every local trace, from the same d_records as
+ * agft_replay ([n_traces][n_steps][128 B]).  ACCUMULATES (+=) into caller-zeroed buffers:
+ *   d_S  [n_traces][K][3]  Σ_t E, Σ_t TPOT, Σ_t EDP per arm (left-to-right in t)
+ *   d_SP [n_traces][5][K]  Σ_t EDP per Table-1 prototype and arm
+ *   d_NP [n_traces][5]     windows per prototype
+ *   d_O  [n_traces][2]     Σ_t EDP and Σ_t E at the per-window EDP-minimising arm k°
+ * and writes d_best [n_traces][n_steps] = k° (smallest index on ties), or NULL.
+ * t0 must equal the handle's sweep counter (0 after create/reset; AGFT_E_STATE otherwise),
+ * so that chunked sweeps accumulate in window order.  Independent of tuner state. */
+agft_status agft_sweep(agft_handle h, const void *d_records, uint32_t t0, uint32_t n_steps, double *d_S,
+                       double *d_SP, uint32_t *d_NP, double *d_O, uint8_t *d_best);
+
+/* From the sweep sums: d_koff [n_traces][6] = k_off(r, p) for prototypes p < 5 (0xFF if
+ * prototype p never occurred) and k_off(r) at index 5 (smallest index on ties); and, if
+ * d_regret is not NULL, d_regret [n_tuners][2] = (sum_edp − Σ EDP at k°, sum_edp −
+ * Σ EDP at k_off(r)) for each tuner's current statistics (compare after the same windows). */
+agft_status agft_regret(agft_handle h, const double *d_S, const double *d_SP, const uint32_t *d_NP,
+                        const double *d_O, uint8_t *d_koff, double *d_regret);
+
 /* Frees the host handle only; the caller frees its device buffers. */
 agft_status agft_destroy(agft_handle h);
 

@@ -4,7 +4,8 @@ The Python layer marshals arguments into the C ABI of ``include/agft.h``
 (``libagft.so``, hand-written sm_100a kernels). PyTorch provides device memory,
 streams and process groups only. Names follow the ABI: ``agft_create``,
 ``agft_trace_generate``, ``agft_step``, ``agft_replay``, ``agft_stats``,
-``agft_export_arms``, ``agft_run``, ``agft_destroy``. ``TunerBatch`` bundles them.
+``agft_export_arms``, ``agft_run``, ``agft_sweep``, ``agft_regret``, ``agft_destroy``.
+``TunerBatch`` bundles them.
 """
 from __future__ import annotations
 
@@ -17,7 +18,8 @@ from ._abi import (NO_RECORD, PARAMS_DTYPE, RECORD_BYTES, ROW_WORDS, STATS_DTYPE
                    make_config, make_params)
 
 __all__ = ["agft_workspace_bytes", "agft_create", "agft_reset", "agft_trace_generate", "agft_step", "agft_replay",
-           "agft_stats", "agft_export_arms", "agft_get_step", "agft_run", "agft_destroy",
+           "agft_stats", "agft_export_arms", "agft_get_step", "agft_run", "agft_sweep", "agft_regret",
+           "agft_destroy", "SweepSums",
            "TunerBatch", "make_config", "make_params", "PARAMS_DTYPE", "STATS_DTYPE", "NO_RECORD",
            "RECORD_BYTES", "ROW_WORDS", "AgftError", "lib_path"]
 
@@ -83,6 +85,32 @@ def agft_get_step(h) -> int:
     t = C.c_uint32()
     _abi.check("agft_get_step", _abi.lib().agft_get_step(h, C.byref(t)))
     return t.value
+
+
+def agft_sweep(h, records, t0, n_steps, S, SP, NP, O, best=None):
+    _abi.check("agft_sweep", _abi.lib().agft_sweep(h, _p(records), t0, n_steps, _p(S), _p(SP), _p(NP), _p(O),
+                                                    _p(best)))
+
+
+def agft_regret(h, S, SP, NP, O, koff, regret=None):
+    _abi.check("agft_regret", _abi.lib().agft_regret(h, _p(S), _p(SP), _p(NP), _p(O), _p(koff), _p(regret)))
+
+
+class SweepSums:
+    """Caller-owned ENV.md §5 accumulators for every local trace (zeroed device tensors)."""
+
+    def __init__(self, n_traces: int, n_arms: int, device):
+        import torch
+        self.S = torch.zeros((n_traces, n_arms, 3), dtype=torch.float64, device=device)
+        self.SP = torch.zeros((n_traces, 5, n_arms), dtype=torch.float64, device=device)
+        self.NP = torch.zeros((n_traces, 5), dtype=torch.int32, device=device)
+        self.O = torch.zeros((n_traces, 2), dtype=torch.float64, device=device)
+        self.koff = torch.zeros((n_traces, 6), dtype=torch.uint8, device=device)
+
+    def host(self) -> dict:
+        return {"S": self.S.cpu().numpy(), "SP": self.SP.cpu().numpy(),
+                "NP": self.NP.cpu().numpy().view(np.uint32), "O": self.O.cpu().numpy(),
+                "koff": self.koff.cpu().numpy()}
 
 
 def agft_run(cfg_c, h_params, d_params_buf, n_steps, chunk_steps, workspace, scratch, d_stats_buf,
@@ -174,6 +202,23 @@ class TunerBatch:
         if record and trajs:
             return torch.cat(trajs, 1).numpy(), torch.cat(gaps, 1).numpy()
         return None, None
+
+    def new_sweep(self) -> SweepSums:
+        return SweepSums(self.n_traces, self.cfg["n_arms"], self.device)
+
+    def sweep(self, records, t0: int, n_steps: int, sums: SweepSums, best: bool = False):
+        """ENV.md §5 over windows [t0, t0+n_steps) into ``sums``; returns k° [n_traces][n] if asked."""
+        import torch
+        b = torch.empty((self.n_traces, n_steps), dtype=torch.uint8, device=self.device) if best else None
+        agft_sweep(self.h, records, t0, n_steps, sums.S, sums.SP, sums.NP, sums.O, b)
+        return b
+
+    def regret(self, sums: SweepSums):
+        """Table-6 Offline arms into ``sums.koff`` and per-tuner (window, fixed) regret [n][2]."""
+        import torch
+        out = torch.empty((self.n, 2), dtype=torch.float64, device=self.device)
+        agft_regret(self.h, sums.S, sums.SP, sums.NP, sums.O, sums.koff, out)
+        return out
 
     def stats_tensor(self):
         import torch

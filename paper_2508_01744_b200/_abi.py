@@ -91,6 +91,8 @@ PROTOTYPES = {
     "agft_get_step": (C.c_int, [vp, C.POINTER(u32)]),
     "agft_run": (C.c_int, [C.POINTER(AgftConfig), vp, vp, u32, u32, vp, C.c_size_t, vp, C.c_size_t,
                            vp, vp, vp]),
+    "agft_sweep": (C.c_int, [vp, vp, u32, u32, vp, vp, vp, vp, vp]),
+    "agft_regret": (C.c_int, [vp, vp, vp, vp, vp, vp, vp]),
     "agft_destroy": (C.c_int, [vp]),
     "agft_status_string": (C.c_char_p, [C.c_int]),
 }

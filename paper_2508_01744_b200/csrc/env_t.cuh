@@ -1,0 +1,62 @@
+// env_t.cuh — device pieces of ENV.md §1–§3 shared by the trace kernel (K1) and the
+// offline sweep (K4): Philox4x32-10, the segment prototype, the §3.3 response.
+// (CUDA path only; the oracle has its own, independent implementation.)
+#pragma once
+#include "agft_internal.cuh"
+
+namespace agft {
+
+struct Philox {
+    uint32_t k0, k1;
+    __device__ __forceinline__ uint4 operator()(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3) const
+    {
+        uint32_t a = k0, b = k1;
+#pragma unroll
+        for (int r = 0; r < 10; ++r) {
+            const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+            const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+            const uint32_t n0 = hi1 ^ c1 ^ a, n2 = hi0 ^ c3 ^ b;
+            c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+            a += 0x9E3779B9u;
+            b += 0xBB67AE85u;
+        }
+        return make_uint4(c0, c1, c2, c3);
+    }
+};
+
+__device__ __forceinline__ double unit32(uint32_t v) { return xmul((double)v, 0x1p-32); }
+__device__ __forceinline__ double unit53(uint32_t a, uint32_t b)
+{
+    const uint64_t m = ((uint64_t)a << 21) ^ ((uint64_t)b >> 11);
+    return xmul((double)m, 0x1p-53);
+}
+
+// ENV.md §3.3 response at one frequency (given its §3.1 constants).
+__device__ __forceinline__ void response(const StepRec &r, double dec, double pre, double pw,
+                                         double W, double invW, double q_over, double u_max,
+                                         double u_floor, double p_idle, double &E, double &tpot)
+{
+    const double t_dec = xmul((double)r.I, dec);
+    const double t_pre = xmul((double)r.P, pre);
+    const double busy = xmul(xadd(t_dec, t_pre), r.g);
+    const double u = xmul(busy, invW);
+    const double q = u <= u_max ? xdiv(1.0, xsub(1.0, u)) : xmul(u, q_over);
+    tpot = xmul(xmul(xmul(xadd(dec, xmul(t_pre, r.invIm)), r.g), q), r.nT);
+    double ue = u > 1.0 ? 1.0 : u;
+    ue = ue < u_floor ? u_floor : ue;
+    E = xmul(xmul(xadd(p_idle, xmul(pw, ue)), W), r.nE);
+}
+
+// ENV.md §2.2: the Table-1 prototype of the 10-minute segment holding window t
+__device__ __forceinline__ uint32_t prototype_of(const agft_trace_cfg &c, const Philox &ph, uint32_t t)
+{
+    const uint32_t v = ph(t / c.seg_steps, 1u, 0u, 0u).x >> 24;
+    uint32_t p = 0, cum = 0;
+    for (; p < 5; ++p) {
+        cum += c.weight[p];
+        if (v < cum) break;
+    }
+    return p >= 5 ? 4u : p;
+}
+
+}  // namespace agft

@@ -18,6 +18,7 @@ struct agft_handle_s {
     cudaStream_t side[kNumCls];   // one stream per kernel class: classes of a sub-chunk overlap
     cudaEvent_t fork, join[kNumCls];
     uint32_t t;             // current global step (observe/apply alternate strictly)
+    uint32_t sweep_t;       // next window of the offline sweep (ENV.md §5 accumulation order)
     agft_status sticky;     // AGFT_OK or AGFT_E_CUDA
 };
 
@@ -194,6 +195,7 @@ agft_status agft_create(const agft_config *cfg, const agft_tuner_params *d_param
     h->ws = make_ws(d_workspace, L);
     h->stream = static_cast<cudaStream_t>(stream);
     h->t = 0;
+    h->sweep_t = 0;
     h->sticky = AGFT_OK;
     h->fork = nullptr;
     for (int c = 0; c < kNumCls; ++c) {
@@ -225,7 +227,10 @@ agft_status agft_reset(agft_handle h)
     if (!h) return AGFT_E_INVALID_ARG;
     if (h->sticky != AGFT_OK) return h->sticky;
     agft_status st = cuda_status(h, launch_init(h->ws, h->cfg, h->stream));
-    if (st == AGFT_OK) h->t = 0;
+    if (st == AGFT_OK) {
+        h->t = 0;
+        h->sweep_t = 0;
+    }
     return st;
 }
 
@@ -337,6 +342,26 @@ agft_status agft_export_arms(agft_handle h, uint32_t tuner, double *d_ainv_packe
     if (tuner >= h->cfg.n_tuners) return AGFT_E_INVALID_ARG;
     return cuda_status(h, launch_export(h->ws, tuner, h->cfg.grid.n_arms, h->cfg.d, d_ainv_packed, d_b, d_theta,
                                         d_n, d_rbar, d_ebar, d_active_mask, h->stream));
+}
+
+agft_status agft_sweep(agft_handle h, const void *d_records, uint32_t t0, uint32_t n_steps, double *d_S,
+                       double *d_SP, uint32_t *d_NP, double *d_O, uint8_t *d_best)
+{
+    if (!h || !d_records || !d_S || !d_SP || !d_NP || !d_O) return AGFT_E_INVALID_ARG;
+    if (h->sticky != AGFT_OK) return h->sticky;
+    if (t0 != h->sweep_t) return AGFT_E_STATE;
+    agft_status st = cuda_status(h, launch_sweep(h->ws, h->cfg, d_records, t0, n_steps, d_S, d_SP, d_NP, d_O,
+                                                 d_best, h->stream));
+    if (st == AGFT_OK) h->sweep_t += n_steps;
+    return st;
+}
+
+agft_status agft_regret(agft_handle h, const double *d_S, const double *d_SP, const uint32_t *d_NP,
+                        const double *d_O, uint8_t *d_koff, double *d_regret)
+{
+    if (!h || !d_S || !d_SP || !d_NP || !d_O || !d_koff) return AGFT_E_INVALID_ARG;
+    if (h->sticky != AGFT_OK) return h->sticky;
+    return cuda_status(h, launch_regret(h->ws, h->cfg, d_S, d_SP, d_NP, d_O, d_koff, d_regret, h->stream));
 }
 
 agft_status agft_get_step(agft_handle h, uint32_t *t)

@@ -1,0 +1,235 @@
+// sweep.cu — K4: the offline frequency sweep of ENV.md §5 (
+// P:257-262 "we iterated through all core frequencies … and calculated the corresponding
+// EDP", Table 6 P:550-567 Offline vs Online) and K5: per-tuner regret against it.
+//
+// K4 mapping: one CTA per trace, one thread per arm (128 slots, K ≤ 128).  Windows are
+// processed in tiles of 32: the tile's step records (4 KB) are staged in shared memory and
+// broadcast to every arm thread; each thread evaluates ENV-R at its frequency for the 32
+// windows, adding E, TPOT, EDP into its per-arm sums in ascending t (ENV.md §5's
+// left-to-right order, so chunked sweeps equal one sweep) and the EDP into the sum of the
+// window's prototype (a block-uniform branch).  The tile's EDPs go to shared memory; each
+// warp then takes 8 windows and finds k° (smallest arm index on ties) with a lane-local
+// pass over 4 arms and a 5-level shuffle argmin; one thread adds the tile's oracle EDP and
+// energy in window order.  FP64-ALU bound: ~22 FP64 operations per (window, arm), the
+// record read once per (trace, window) for 107 arms.
+#include "env_t.cuh"
+
+namespace agft {
+
+namespace {
+
+constexpr int kTile = 32;
+constexpr int kThreads = 128;
+constexpr uint32_t kNoArm = 0xFFu;
+constexpr double kInf = __builtin_huge_val();
+
+struct SweepArgs {
+    const StepRec *records;   // [n_traces][n_steps]
+    double *S;                // [n_traces][K][3]   ΣE, ΣTPOT, ΣEDP
+    double *SP;               // [n_traces][5][K]   Σ EDP per prototype
+    uint32_t *NP;             // [n_traces][5]
+    double *O;                // [n_traces][2]      Σ EDP°, Σ E°
+    uint8_t *best;            // [n_traces][n_steps] k°, or null
+    const EnvConsts *env;
+    agft_trace_cfg tc;
+    uint64_t seed;
+    uint32_t trace_base, n_traces, t0, n_steps, K;
+    double W, p_idle, u_floor, u_max;
+};
+
+__global__ void __launch_bounds__(kThreads) sweep_kernel(const __grid_constant__ SweepArgs a)
+{
+    __shared__ __align__(16) StepRec s_rec[kTile];
+    __shared__ double s_edp[kTile][kThreads];
+    __shared__ uint32_t s_proto[kTile];
+    __shared__ double s_oe[kTile], s_oE[kTile];
+    const uint32_t r = blockIdx.x;                                    // local trace
+    const int k = threadIdx.x, lane = k & 31, warp = k >> 5;
+    const bool arm = (uint32_t)k < a.K;
+    const EnvConsts &ec = *a.env;
+    const double dec = arm ? ec.dec[k] : 0.0, pre = arm ? ec.pre[k] : 0.0, pw = arm ? ec.pw[k] : 0.0;
+    const double invW = ec.invW, q_over = ec.q_over;
+    const Philox ph{(uint32_t)a.seed ^ (a.trace_base + r), (uint32_t)(a.seed >> 32)};
+
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, sp[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    if (arm) {
+        const double *S = a.S + ((size_t)r * a.K + k) * 3;
+        s0 = S[0];
+        s1 = S[1];
+        s2 = S[2];
+#pragma unroll
+        for (int p = 0; p < 5; ++p) sp[p] = a.SP[((size_t)r * 5 + p) * a.K + k];
+    }
+    double o0 = 0.0, o1 = 0.0;
+    uint32_t np[5] = {0u, 0u, 0u, 0u, 0u};
+    if (k == 0) {
+        o0 = a.O[2 * r];
+        o1 = a.O[2 * r + 1];
+#pragma unroll
+        for (int p = 0; p < 5; ++p) np[p] = a.NP[r * 5 + p];
+    }
+    const StepRec *rp = a.records + (size_t)r * a.n_steps;
+
+    for (uint32_t base = 0; base < a.n_steps; base += kTile) {
+        const int nw = (int)min((uint32_t)kTile, a.n_steps - base);
+        // ---- stage the tile's records (coalesced 16-B loads) and prototypes
+        {
+            const uint4 *src = reinterpret_cast<const uint4 *>(rp + base);
+            uint4 *dst = reinterpret_cast<uint4 *>(s_rec);
+            for (int q = k; q < nw * 8; q += kThreads) dst[q] = __ldg(src + q);
+            if (k < nw) s_proto[k] = prototype_of(a.tc, ph, a.t0 + base + (uint32_t)k);
+        }
+        __syncthreads();
+        // ---- ENV-R at this thread's frequency for every window of the tile (ENV.md §3.3)
+        for (int w = 0; w < nw; ++w) {
+            double edp = kInf;
+            if (arm) {
+                double E, tpot;
+                response(s_rec[w], dec, pre, pw, a.W, invW, q_over, a.u_max, a.u_floor, a.p_idle, E, tpot);
+                edp = xmul(E, tpot);
+                s0 = xadd(s0, E);
+                s1 = xadd(s1, tpot);
+                s2 = xadd(s2, edp);
+                switch (s_proto[w]) {                                 // block-uniform
+                case 0: sp[0] = xadd(sp[0], edp); break;
+                case 1: sp[1] = xadd(sp[1], edp); break;
+                case 2: sp[2] = xadd(sp[2], edp); break;
+                case 3: sp[3] = xadd(sp[3], edp); break;
+                default: sp[4] = xadd(sp[4], edp); break;
+                }
+            }
+            s_edp[w][k] = edp;
+        }
+        __syncthreads();
+        // ---- per-window oracle arm k° (smallest index on ties), 8 windows per warp
+        for (int j = 0; j < kTile / 4; ++j) {
+            const int w = warp * (kTile / 4) + j;
+            if (w >= nw) break;                                           // warp-uniform
+            double bv = s_edp[w][lane];
+            int bk = lane;
+#pragma unroll
+            for (int q = 1; q < kThreads / 32; ++q) {
+                const double v = s_edp[w][lane + 32 * q];
+                if (v < bv) {
+                    bv = v;
+                    bk = lane + 32 * q;
+                }
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                const double ov = __shfl_xor_sync(kFull, bv, off);
+                const int ok = __shfl_xor_sync(kFull, bk, off);
+                if (ov < bv || (ov == bv && ok < bk)) {
+                    bv = ov;
+                    bk = ok;
+                }
+            }
+            if (lane == j) {                                              // energy at k°, bit-identical
+                double E, tpot;
+                response(s_rec[w], ec.dec[bk], ec.pre[bk], ec.pw[bk], a.W, invW, q_over, a.u_max, a.u_floor,
+                         a.p_idle, E, tpot);
+                s_oe[w] = bv;
+                s_oE[w] = E;
+                if (a.best) a.best[(size_t)r * a.n_steps + base + w] = (uint8_t)bk;
+            }
+        }
+        __syncthreads();
+        if (k == 0) {                                                     // ENV.md §5: in window order
+            for (int w = 0; w < nw; ++w) {
+                o0 = xadd(o0, s_oe[w]);
+                o1 = xadd(o1, s_oE[w]);
+                np[s_proto[w]] += 1u;
+            }
+        }
+    }
+    if (arm) {
+        double *S = a.S + ((size_t)r * a.K + k) * 3;
+        S[0] = s0;
+        S[1] = s1;
+        S[2] = s2;
+#pragma unroll
+        for (int p = 0; p < 5; ++p) a.SP[((size_t)r * 5 + p) * a.K + k] = sp[p];
+    }
+    if (k == 0) {
+        a.O[2 * r] = o0;
+        a.O[2 * r + 1] = o1;
+#pragma unroll
+        for (int p = 0; p < 5; ++p) a.NP[r * 5 + p] = np[p];
+    }
+}
+
+// K5a: Table-6 "Offline" arms — k_off(r, p) for p < 5 (kNoArm if the prototype never
+// occurred) and k_off(r) in slot 5; smallest index on ties
+__global__ void offline_kernel(const double *S, const double *SP, const uint32_t *NP, uint32_t n_traces, uint32_t K,
+                               uint8_t *koff)
+{
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_traces * 6u) return;
+    const uint32_t r = i / 6u, p = i % 6u;
+    if (p < 5 && NP[r * 5 + p] == 0u) {
+        koff[i] = (uint8_t)kNoArm;
+        return;
+    }
+    uint32_t kb = 0;
+    double bv = 0.0;
+    for (uint32_t k = 0; k < K; ++k) {
+        const double v = p < 5 ? SP[((size_t)r * 5 + p) * K + k] : S[((size_t)r * K + k) * 3 + 2];
+        if (k == 0 || v < bv) {
+            bv = v;
+            kb = k;
+        }
+    }
+    koff[i] = (uint8_t)kb;
+}
+
+// K5b: per-tuner regret against the per-window oracle and the best fixed arm (ENV.md §5)
+__global__ void regret_kernel(Ws w, uint32_t N, uint32_t K, const double *S, const double *O, const uint8_t *koff,
+                              double *regret)
+{
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    const uint32_t r = w.params[i].trace_id;
+    const double e = w.acc[i].sum_edp;
+    regret[2 * (size_t)i] = xsub(e, O[2 * r]);
+    regret[2 * (size_t)i + 1] = xsub(e, S[((size_t)r * K + koff[r * 6 + 5]) * 3 + 2]);
+}
+
+}  // namespace
+
+cudaError_t launch_sweep(const Ws &w, const agft_config &c, const void *records, uint32_t t0, uint32_t n_steps,
+                         double *S, double *SP, uint32_t *NP, double *O, uint8_t *best, cudaStream_t s)
+{
+    if (n_steps == 0) return cudaSuccess;
+    SweepArgs a;
+    a.records = static_cast<const StepRec *>(records);
+    a.S = S;
+    a.SP = SP;
+    a.NP = NP;
+    a.O = O;
+    a.best = best;
+    a.env = w.env;
+    a.tc = c.trace;
+    a.seed = c.env_seed;
+    a.trace_base = c.trace_base;
+    a.n_traces = c.n_traces;
+    a.t0 = t0;
+    a.n_steps = n_steps;
+    a.K = c.grid.n_arms;
+    a.W = c.env.window_s;
+    a.p_idle = c.env.p_idle;
+    a.u_floor = c.env.u_floor;
+    a.u_max = c.env.u_max;
+    sweep_kernel<<<c.n_traces, kThreads, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_regret(const Ws &w, const agft_config &c, const double *S, const double *SP, const uint32_t *NP,
+                          const double *O, uint8_t *koff, double *regret, cudaStream_t s)
+{
+    const uint32_t nk = c.n_traces * 6u;
+    offline_kernel<<<(nk + 127) / 128, 128, 0, s>>>(S, SP, NP, c.n_traces, c.grid.n_arms, koff);
+    if (regret) regret_kernel<<<(c.n_tuners + 255) / 256, 256, 0, s>>>(w, c.n_tuners, c.grid.n_arms, S, O, koff, regret);
+    return cudaGetLastError();
+}
+
+}  // namespace agft

@@ -4,50 +4,9 @@
 // One thread per (trace, step): six Philox4x32-10 draws (ENV.md §1-2), integer
 // row synthesis, then the record of ENV.md §3.2 including the f_max baseline
 // response.  HBM-write bound: 128 B (+48 B raw) per (trace, step).
-#include "agft_internal.cuh"
+#include "env_t.cuh"
 
 namespace agft {
-
-struct Philox {
-    uint32_t k0, k1;
-    __device__ __forceinline__ uint4 operator()(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3) const
-    {
-        uint32_t a = k0, b = k1;
-#pragma unroll
-        for (int r = 0; r < 10; ++r) {
-            const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
-            const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
-            const uint32_t n0 = hi1 ^ c1 ^ a, n2 = hi0 ^ c3 ^ b;
-            c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
-            a += 0x9E3779B9u;
-            b += 0xBB67AE85u;
-        }
-        return make_uint4(c0, c1, c2, c3);
-    }
-};
-
-__device__ __forceinline__ double unit32(uint32_t v) { return xmul((double)v, 0x1p-32); }
-__device__ __forceinline__ double unit53(uint32_t a, uint32_t b)
-{
-    const uint64_t m = ((uint64_t)a << 21) ^ ((uint64_t)b >> 11);
-    return xmul((double)m, 0x1p-53);
-}
-
-// ENV.md §3.3 response at one frequency (given its §3.1 constants).
-__device__ __forceinline__ void response(const StepRec &r, double dec, double pre, double pw,
-                                         double W, double invW, double q_over, double u_max,
-                                         double u_floor, double p_idle, double &E, double &tpot)
-{
-    const double t_dec = xmul((double)r.I, dec);
-    const double t_pre = xmul((double)r.P, pre);
-    const double busy = xmul(xadd(t_dec, t_pre), r.g);
-    const double u = xmul(busy, invW);
-    const double q = u <= u_max ? xdiv(1.0, xsub(1.0, u)) : xmul(u, q_over);
-    tpot = xmul(xmul(xmul(xadd(dec, xmul(t_pre, r.invIm)), r.g), q), r.nT);
-    double ue = u > 1.0 ? 1.0 : u;
-    ue = ue < u_floor ? u_floor : ue;
-    E = xmul(xmul(xadd(p_idle, xmul(pw, ue)), W), r.nE);
-}
 
 __global__ void __launch_bounds__(256) trace_kernel(const __grid_constant__ TraceArgs a)
 {
@@ -61,14 +20,7 @@ __global__ void __launch_bounds__(256) trace_kernel(const __grid_constant__ Trac
     const Philox ph{(uint32_t)a.seed ^ r, (uint32_t)(a.seed >> 32)};
 
     uint32_t pattern = c.pattern_mode < 3 ? c.pattern_mode : (c.pattern_mode == 3 ? r % 3u : 1u + r % 2u);
-    // segment prototype (Table 1 mix)
-    const uint32_t v = ph(t / c.seg_steps, 1u, 0u, 0u).x >> 24;
-    uint32_t p = 0, cum = 0;
-    for (; p < 5; ++p) {
-        cum += c.weight[p];
-        if (v < cum) break;
-    }
-    if (p >= 5) p = 4;
+    const uint32_t p = prototype_of(c, ph, t);                // segment prototype (Table 1 mix)
     // rate multiplier (diurnal knots, burst)
     double m = 1.0;
     if (pattern >= 1) {

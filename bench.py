@@ -25,6 +25,8 @@ import sys
 import threading
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -126,6 +128,8 @@ def main():
     ap.add_argument("--scaling", default=None, choices=["weak", "strong"],
                     help="weak: every rank runs the full config (default for C1-C4); strong: split it (C5)")
     ap.add_argument("--backend", default="nccl", help="process-group backend for N > 1 (nccl; gloo for tests)")
+    ap.add_argument("--workload", default="replay", choices=["replay", "sweep"],
+                    help="replay: the tuner hot path (north-star metric); sweep: ENV.md §5 offline sweep")
     args = ap.parse_args()
     if args.scaling is None:
         args.scaling = "strong" if args.config == "C5" else "weak"
@@ -142,6 +146,8 @@ def main():
 
     if args.impl == "reference":
         return reference_arm(args, cfg, rank, world)
+    if args.workload == "sweep":
+        return sweep_bench(args, cfg, rank, world, local)
 
     import numpy as np
     import torch
@@ -256,6 +262,94 @@ def main():
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:
+        dist.destroy_process_group()
+
+
+SWEEP_FLOPS = 21   # ENV.md §3.3 without TTFT (13 mul/add, 1 sub, 1 div) + 4 accumulations (§5)
+
+
+def sweep_bench(args, cfg, rank, world, local):
+    """ENV.md §5 offline sweep over the whole day (every trace × every arm × every window):
+    one step = trace records (K1) + sweep (K4) for all chunks + Table-6 arms (K5a)."""
+    import torch
+    from paper_2508_01744_b200 import TunerBatch
+    from paper_2508_01744_b200 import shard
+    torch.cuda.set_device(local % max(1, torch.cuda.device_count()))
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group(args.backend, device_id=torch.device("cuda", local)) if args.backend == "nccl" \
+            else dist.init_process_group(args.backend)
+    sh = shard.plan(cfg, world, rank, args.scaling)
+    R, T, K = sh.n_traces, cfg["T"], cfg["n_arms"]
+    c = dict(cfg, n_tuners=sh.n_tuners, n_traces=R)
+    tb = TunerBatch(c, sh.params, device=f"cuda:{local}", trace_base=sh.trace_base)
+    stream = torch.cuda.current_stream()
+    chunk = min(CHUNK, T)
+    records = tb.new_records(chunk)
+    ev = []
+
+    def one(timed):
+        sums = tb.new_sweep()
+        tb.reset()
+        t = 0
+        while t < T:
+            m = min(chunk, T - t)
+            tb.generate(t, m, records)
+            if timed:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                tb.sweep(records, t, m, sums)
+                e1.record(stream)
+                ev.append((e0, e1, m))
+            else:
+                tb.sweep(records, t, m, sums)
+            t += m
+        tb.regret(sums)
+        return sums
+
+    for _ in range(args.warmup):
+        one(False)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    for _ in range(args.steps):
+        sums = one(True)
+    end.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = start.elapsed_time(end)
+    if world > 1:
+        import torch.distributed as dist
+        t_ = torch.tensor([ms], dtype=torch.float64, device="cuda" if args.backend == "nccl" else "cpu")
+        dist.all_reduce(t_, op=dist.ReduceOp.MAX)
+        ms = float(t_.item())
+    k_ms = sum(a.elapsed_time(b) for a, b, _ in ev)
+    evals = float(R) * K * T
+    achieved = evals * SWEEP_FLOPS * args.steps / (k_ms / 1e3) / 1e12
+    pk = peaks()
+    sm_mhz = float(pk.get("sm_max_mhz", 1965.0))
+    peak_fp64 = N_SM * FP64_UNITS_PER_SM * 2 * sm_mhz * 1e6 / 1e12
+    h = sums.host()
+    out = {"metric": "offline-sweep window-arm evaluations/s (ENV.md §5)", "value": round(evals * world * args.steps / (ms / 1e3), 1),
+           "unit": "window-arm evals/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True, "scaling": args.scaling,
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": f"{args.config} sweep: {R} traces × {K} arms × {T} windows",
+                      "traces_per_gpu": R, "arms": K, "T": T, "chunk": chunk},
+           "roofline": {"bound": "alu", "achieved": round(achieved, 4), "peak": round(peak_fp64, 2),
+                        "unit": "TFLOP/s", "frac": round(achieved / peak_fp64, 5), "traffic": None,
+                        "kernel": "sweep_kernel", "kernel_share": round(k_ms / ms, 4),
+                        "flops_per_eval": SWEEP_FLOPS,
+                        "peak_source": "derived: 148 SM × 64 FP64 FMA/clk × 2 × sm_max_mhz (DESIGN.md §5)"},
+           "clocks": clk, "gpu_launches": args.steps * (2 * ((T + chunk - 1) // chunk) + 2),
+           "check": {"windows_counted": int(h["NP"].sum()) == R * T,
+                     "oracle_le_fixed": bool(np.all(h["O"][:, 0][:, None] <= h["S"][:, :, 2]))}}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
         dist.destroy_process_group()
 
 

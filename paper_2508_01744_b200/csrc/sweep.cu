@@ -5,11 +5,12 @@
 // K4 mapping: one CTA per trace, one thread per arm (128 slots, K ≤ 128).  Windows are
 // processed in tiles of 32: the tile's step records (4 KB) are staged in shared memory and
 // broadcast to every arm thread; each thread evaluates ENV-R at its frequency for the 32
-// windows, adding E, TPOT, EDP into its per-arm sums in ascending t (ENV.md §5's
-// left-to-right order, so chunked sweeps equal one sweep) and the EDP into the sum of the
-// window's prototype (a block-uniform branch).  The tile's EDPs go to shared memory; each
+// windows (kIlp independent evaluations in flight), adding E, TPOT, EDP into its per-arm
+// sums in ascending t (ENV.md §5's left-to-right order, so chunked sweeps equal one sweep)
+// and the EDP into the running sum of the window's prototype (runs split at segment
+// boundaries, so the prototype is block-uniform per run).  The tile's EDPs go to shared memory; each
 // warp then takes 8 windows and finds k° (smallest arm index on ties) with a lane-local
-// pass over 4 arms and a 5-level shuffle argmin; one thread adds the tile's oracle EDP and
+// pass over 4 arms and three warp min-reductions on the EDP bit patterns; one thread adds the tile's oracle EDP and
 // energy in window order.  FP64-ALU bound: ~22 FP64 operations per (window, arm), the
 // record read once per (trace, window) for 107 arms.
 #include "env_t.cuh"
@@ -20,6 +21,10 @@ namespace {
 
 constexpr int kTile = 32;
 constexpr int kThreads = 128;
+#ifndef AGFT_SWEEP_ILP
+#define AGFT_SWEEP_ILP 8
+#endif
+constexpr int kIlp = AGFT_SWEEP_ILP;          // independent ENV-R evaluations in flight per thread
 constexpr uint32_t kNoArm = 0xFFu;
 constexpr double kInf = __builtin_huge_val();
 
@@ -41,7 +46,6 @@ __global__ void __launch_bounds__(kThreads) sweep_kernel(const __grid_constant__
 {
     __shared__ __align__(16) StepRec s_rec[kTile];
     __shared__ double s_edp[kTile][kThreads];
-    __shared__ uint32_t s_proto[kTile];
     __shared__ double s_oe[kTile], s_oE[kTile];
     const uint32_t r = blockIdx.x;                                    // local trace
     const int k = threadIdx.x, lane = k & 31, warp = k >> 5;
@@ -77,31 +81,49 @@ __global__ void __launch_bounds__(kThreads) sweep_kernel(const __grid_constant__
             const uint4 *src = reinterpret_cast<const uint4 *>(rp + base);
             uint4 *dst = reinterpret_cast<uint4 *>(s_rec);
             for (int q = k; q < nw * 8; q += kThreads) dst[q] = __ldg(src + q);
-            if (k < nw) s_proto[k] = prototype_of(a.tc, ph, a.t0 + base + (uint32_t)k);
         }
         __syncthreads();
-        // ---- ENV-R at this thread's frequency for every window of the tile (ENV.md §3.3)
-        for (int w = 0; w < nw; ++w) {
-            double edp = kInf;
-            if (arm) {
-                double E, tpot;
-                response(s_rec[w], dec, pre, pw, a.W, invW, q_over, a.u_max, a.u_floor, a.p_idle, E, tpot);
-                edp = xmul(E, tpot);
-                s0 = xadd(s0, E);
-                s1 = xadd(s1, tpot);
-                s2 = xadd(s2, edp);
-                switch (s_proto[w]) {                                 // block-uniform
-                case 0: sp[0] = xadd(sp[0], edp); break;
-                case 1: sp[1] = xadd(sp[1], edp); break;
-                case 2: sp[2] = xadd(sp[2], edp); break;
-                case 3: sp[3] = xadd(sp[3], edp); break;
-                default: sp[4] = xadd(sp[4], edp); break;
+        // ---- ENV-R at this thread's frequency for every window of the tile (ENV.md §3.3):
+        // kIlp independent evaluations in flight, then the in-order accumulation.  Windows of
+        // one 10-minute segment share a prototype, so a tile holds at most two prototype runs
+        // (seg_steps ≥ kTile); each run accumulates into one register copied in and out.
+        int w = 0;
+        while (w < nw) {                                                  // block-uniform runs
+            const uint32_t t = a.t0 + base + (uint32_t)w;
+            const uint32_t p = prototype_of(a.tc, ph, t);
+            const int wend = w + (int)min((uint32_t)(nw - w), a.tc.seg_steps - t % a.tc.seg_steps);
+            if (k == 0) np[p] += (uint32_t)(wend - w);
+            double cur = p == 0 ? sp[0] : p == 1 ? sp[1] : p == 2 ? sp[2] : p == 3 ? sp[3] : sp[4];
+            for (; w < wend; w += kIlp) {
+                double E[kIlp], tp[kIlp], ed[kIlp];
+#pragma unroll
+                for (int j = 0; j < kIlp; ++j) {
+                    const int wj = w + j < wend ? w + j : w;
+                    response(s_rec[wj], dec, pre, pw, a.W, invW, q_over, a.u_max, a.u_floor, a.p_idle, E[j], tp[j]);
+                    ed[j] = xmul(E[j], tp[j]);
                 }
+#pragma unroll
+                for (int j = 0; j < kIlp; ++j)
+                    if (w + j < wend) {
+                        s_edp[w + j][k] = arm ? ed[j] : kInf;
+                        s0 = xadd(s0, E[j]);
+                        s1 = xadd(s1, tp[j]);
+                        s2 = xadd(s2, ed[j]);
+                        cur = xadd(cur, ed[j]);
+                    }
             }
-            s_edp[w][k] = edp;
+            w = wend;
+            if (p == 0) sp[0] = cur;
+            else if (p == 1) sp[1] = cur;
+            else if (p == 2) sp[2] = cur;
+            else if (p == 3) sp[3] = cur;
+            else sp[4] = cur;
         }
         __syncthreads();
-        // ---- per-window oracle arm k° (smallest index on ties), 8 windows per warp
+        // ---- per-window oracle arm k° (smallest index on ties), 8 windows per warp.  EDP > 0
+        // (ENV.md §3.3) and inactive slots hold +inf, so doubles order like their bit
+        // patterns: min of the high words, then of the low words among the ties, then the
+        // smallest arm index among exact ties (three warp reductions, no shuffle tree).
         for (int j = 0; j < kTile / 4; ++j) {
             const int w = warp * (kTile / 4) + j;
             if (w >= nw) break;                                           // warp-uniform
@@ -115,22 +137,18 @@ __global__ void __launch_bounds__(kThreads) sweep_kernel(const __grid_constant__
                     bk = lane + 32 * q;
                 }
             }
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-                const double ov = __shfl_xor_sync(kFull, bv, off);
-                const int ok = __shfl_xor_sync(kFull, bk, off);
-                if (ov < bv || (ov == bv && ok < bk)) {
-                    bv = ov;
-                    bk = ok;
-                }
-            }
+            const uint64_t bits = (uint64_t)__double_as_longlong(bv);
+            const uint32_t hi = (uint32_t)(bits >> 32), lo = (uint32_t)bits;
+            const uint32_t mhi = __reduce_min_sync(kFull, hi);
+            const uint32_t mlo = __reduce_min_sync(kFull, hi == mhi ? lo : 0xFFFFFFFFu);
+            const uint32_t kmin = __reduce_min_sync(kFull, (hi == mhi && lo == mlo) ? (uint32_t)bk : 0xFFFFFFFFu);
             if (lane == j) {                                              // energy at k°, bit-identical
                 double E, tpot;
-                response(s_rec[w], ec.dec[bk], ec.pre[bk], ec.pw[bk], a.W, invW, q_over, a.u_max, a.u_floor,
-                         a.p_idle, E, tpot);
-                s_oe[w] = bv;
+                response(s_rec[w], ec.dec[kmin], ec.pre[kmin], ec.pw[kmin], a.W, invW, q_over, a.u_max,
+                         a.u_floor, a.p_idle, E, tpot);
+                s_oe[w] = __longlong_as_double((long long)(((uint64_t)mhi << 32) | mlo));
                 s_oE[w] = E;
-                if (a.best) a.best[(size_t)r * a.n_steps + base + w] = (uint8_t)bk;
+                if (a.best) a.best[(size_t)r * a.n_steps + base + w] = (uint8_t)kmin;
             }
         }
         __syncthreads();
@@ -138,7 +156,6 @@ __global__ void __launch_bounds__(kThreads) sweep_kernel(const __grid_constant__
             for (int w = 0; w < nw; ++w) {
                 o0 = xadd(o0, s_oe[w]);
                 o1 = xadd(o1, s_oE[w]);
-                np[s_proto[w]] += 1u;
             }
         }
     }

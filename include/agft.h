@@ -40,6 +40,7 @@ extern "C" {
 #define AGFT_POLICY_AUTO 0u         /* re-classify by active-arm count: SOLO (1), SEG<8/16/32>, WIDE (>32) */
 #define AGFT_POLICY_WIDE 1u         /* one warp per tuner for every step (reference schedule) */
 #define AGFT_POLICY_MSEG 2u         /* as AUTO but 2..32 arms on MSEG (arm state streamed from L2) */
+#define AGFT_POLICY_LANE 3u         /* as AUTO but 2..32 arms on LANE (lane per tuner, batched scoring) */
 
 typedef struct agft_handle_s *agft_handle;
 
@@ -93,7 +94,7 @@ typedef struct {
     uint32_t n_traces;        /* R: traces held by this handle (local ids 0..R-1) */
     uint32_t trace_base;      /* global id of local trace 0 (Philox key, ENV.md §1) */
     uint32_t record_slots;    /* rows of d_traj / d_gap in agft_replay (0 = none) */
-    uint32_t kernel_policy;   /* AGFT_POLICY_AUTO, AGFT_POLICY_WIDE or AGFT_POLICY_MSEG */
+    uint32_t kernel_policy;   /* AGFT_POLICY_AUTO, _WIDE, _MSEG or _LANE */
     uint32_t pad0;
     agft_grid grid;
     agft_prune prune;

@@ -47,6 +47,13 @@ int mseg_g()
     return g;
 }
 
+// AGFT_LANE_EXACT=1: LANE evaluates the canonical pruning tree every window (tests, A/B)
+uint32_t lane_force_exact()
+{
+    const char *e = std::getenv("AGFT_LANE_EXACT");
+    return (e && e[0] == '1') ? 1u : 0u;
+}
+
 void destroy_streams(agft_handle h)
 {
     for (int c = 0; c < kNumCls; ++c) {
@@ -61,7 +68,7 @@ agft_status validate(const agft_config *c)
     if (!c) return AGFT_E_INVALID_ARG;
     if (c->abi_version != AGFT_ABI_VERSION) return AGFT_E_INVALID_ARG;
     if (c->n_tuners == 0 || c->n_traces == 0) return AGFT_E_INVALID_ARG;
-    if (c->kernel_policy > AGFT_POLICY_MSEG) return AGFT_E_INVALID_ARG;
+    if (c->kernel_policy > AGFT_POLICY_LANE) return AGFT_E_INVALID_ARG;
     const agft_grid &g = c->grid;
     if (g.n_arms == 0) return AGFT_E_EMPTY_ARMS;
     if (g.f_step_mhz == 0 || g.n_arms > AGFT_MAX_ARMS || g.f_min_mhz == 0) return AGFT_E_INVALID_GRID;
@@ -115,7 +122,7 @@ agft_status cuda_status(agft_handle h, cudaError_t e)
 ReplayArgs replay_args(agft_handle h, const void *records, uint32_t t0, uint32_t n_steps)
 {
     const agft_config &c = h->cfg;
-    ReplayArgs a;
+    ReplayArgs a{};
     std::memset(&a, 0, sizeof(a));
     a.w = h->ws;
     a.records = static_cast<const StepRec *>(records);
@@ -279,6 +286,8 @@ static agft_status run_steps(agft_handle h, const void *d_records, uint32_t t0, 
             e = launch_replay(a, c.d, h->stream);
         } else {
             const bool split = c.kernel_policy != AGFT_POLICY_MSEG;
+            const bool lane = c.kernel_policy == AGFT_POLICY_LANE && lane_supported(c.d);
+            a.force_exact = lane_force_exact();
             e = launch_classify(h->ws, c.n_tuners, split, h->stream);
             if (e == cudaSuccess) e = cudaEventRecord(h->fork, h->stream);
             for (int k = 0; k < kNumCls && e == cudaSuccess; ++k) {
@@ -289,9 +298,10 @@ static agft_status run_steps(agft_handle h, const void *d_records, uint32_t t0, 
                 if (e != cudaSuccess) break;
                 switch (k) {
                 case kClsWide: e = launch_replay(ak, c.d, h->side[k]); break;
-                case kClsSeg32: e = split ? launch_seg2(ak, c.d, 16, h->side[k]) : launch_mseg(ak, c.d, mseg_g(), h->side[k]); break;
-                case kClsSeg16: e = launch_seg2(ak, c.d, 8, h->side[k]); break;
-                case kClsSeg8: e = launch_seg2(ak, c.d, 4, h->side[k]); break;
+                case kClsSeg32: e = lane ? launch_lane(ak, c.d, 32, h->side[k])
+                                  : split ? launch_seg2(ak, c.d, 16, h->side[k]) : launch_mseg(ak, c.d, mseg_g(), h->side[k]); break;
+                case kClsSeg16: e = lane ? launch_lane(ak, c.d, 16, h->side[k]) : launch_seg2(ak, c.d, 8, h->side[k]); break;
+                case kClsSeg8: e = lane ? launch_lane(ak, c.d, 8, h->side[k]) : launch_seg2(ak, c.d, 4, h->side[k]); break;
                 case kClsSeg64: e = launch_seg2(ak, c.d, 32, h->side[k]); break;
                 default: e = launch_solo(ak, c.d, h->side[k]); break;
                 }

@@ -49,6 +49,7 @@ class OrcConfig(C.Structure):
         ("lambda0", f64), ("burst_mult", f64), ("t_iter0", f64), ("t_iter1", f64), ("e2e0", f64),
         ("tau_ref", f64),
         ("conc_mult", f64 * 5), ("hit_rate", f64 * 5), ("knot", f64 * 24),
+        ("ph_enable", u32), ("ph_window", u32), ("ph_delta", f64), ("ph_lambda", f64),
     ]
 
 
@@ -63,7 +64,8 @@ class OrcStats(C.Structure):
                 ("n_pruned_hist", u32), ("n_pruned_cascade", u32), ("near_tie_steps", u32),
                 ("follow_violations", u32),
                 ("sum_energy", f64), ("sum_tpot", f64), ("sum_ttft", f64), ("sum_edp", f64),
-                ("sum_reward", f64), ("base_energy", f64), ("base_edp", f64), ("max_viol_rel", f64)]
+                ("sum_reward", f64), ("base_energy", f64), ("base_edp", f64), ("max_viol_rel", f64),
+                ("exploit_steps", u32), ("ph_alarms", u32), ("first_exploit_t", u32), ("phase", u32)]
 
 
 MAXK, MAXD = 128, 7

@@ -379,7 +379,35 @@ typedef struct {
     int active[ORC_MAX_ARMS];
     double window[ORC_MAX_WINDOW];     /* chronological ring of EDPs */
     uint32_t wcount, whead;
+    /* Page-Hinkley detector (ENV.md §4.10) */
+    uint32_t phase, ph_quiet, ph_n;
+    double ph_mean, ph_cum, ph_min;
 } tuner_state;
+
+/* ENV.md §4.10, observe_reward: classical Page-Hinkley on the reward
+ * stream; an alarm (cum - min > λ) resets the detector and re-enters Exploration; W quiet
+ * observations since the last reset enter Exploitation. */
+static void ph_observe(const orc_config *c, tuner_state *S, double r, uint32_t t, orc_stats *st)
+{
+    S->ph_n += 1;
+    double inv = 1.0 / (double)S->ph_n;
+    S->ph_mean = S->ph_mean + (r - S->ph_mean) * inv;
+    S->ph_cum = S->ph_cum + ((r - S->ph_mean) - c->ph_delta);
+    if (S->ph_cum < S->ph_min) S->ph_min = S->ph_cum;
+    S->ph_quiet += 1;
+    if (S->ph_cum - S->ph_min > c->ph_lambda) {          /* drift alarm */
+        st->ph_alarms += 1;
+        S->ph_quiet = 0;
+        S->ph_n = 0;
+        S->ph_mean = 0.0;
+        S->ph_cum = 0.0;
+        S->ph_min = 0.0;
+        S->phase = 0;
+    } else if (S->phase == 0 && S->ph_quiet >= c->ph_window) {   /* stable: Exploitation */
+        S->phase = 1;
+        if (st->first_exploit_t == ORC_NEVER) st->first_exploit_t = t;
+    }
+}
 
 /* a8 reward (AMB-3): r = clip(1 - EDP/median(window), lo, hi); 0 on an empty window */
 double orc_reward(double edp, const double *window, uint32_t n, double clip_lo, double clip_hi)
@@ -417,6 +445,7 @@ int orc_run_tuner_ex(const orc_config *c, const orc_tuner *tu, uint32_t T, const
     }
     memset(st, 0, sizeof(*st));
     st->traj_hash = 0xcbf29ce484222325ull;
+    st->first_exploit_t = ORC_NEVER;
 
     /* f_max baseline response constants are folded into orc_env_response */
     uint32_t row[ORC_ROW_WORDS];
@@ -434,6 +463,10 @@ int orc_run_tuner_ex(const orc_config *c, const orc_tuner *tu, uint32_t T, const
             for (uint32_t i = 0; i < 7; ++i) x[i] = srec.x[i];
         }
         double alpha = tu->alpha0 / sqrt(1.0 + (double)t / c->tau);   /* a3, AMB-1 */
+        if (c->ph_enable && S->phase == 1) {                          /* Exploitation: Eq. 2 greedy */
+            alpha = 0.0;
+            st->exploit_steps += 1;
+        }
 
         uint32_t n_act = 0;
         for (uint32_t k = 0; k < K; ++k) n_act += S->active[k] ? 1u : 0u;
@@ -496,6 +529,7 @@ int orc_run_tuner_ex(const orc_config *c, const orc_tuner *tu, uint32_t T, const
         double E = resp[0], tpot = resp[1], ttft = resp[2], edp = resp[3];
         double r = orc_reward(edp, S->window, S->wcount, c->clip_lo, c->clip_hi);
         if (inj && inj->reward) r = inj->reward[(size_t)t * K + kstar];
+        if (c->ph_enable) ph_observe(c, S, r, t, st);                /* §4.10, after a8 */
         if (S->wcount < c->median_window) {
             S->window[S->wcount++] = edp;
         } else {                                   /* overwrite the oldest */
@@ -601,6 +635,7 @@ int orc_run_tuner_ex(const orc_config *c, const orc_tuner *tu, uint32_t T, const
     uint32_t na = 0;
     for (uint32_t k = 0; k < K; ++k) na += S->active[k] ? 1u : 0u;
     st->n_active = na;
+    st->phase = S->phase;
 
     if (arms_out) {
         memset(arms_out, 0, sizeof(*arms_out));

@@ -42,6 +42,9 @@ typedef struct {
     double W, p_idle, k_lin, k_cube, u_floor, u_max, c_p, c_d, beta, sigma_e, sigma_t;
     double lambda0, burst_mult, t_iter0, t_iter1, e2e0, tau_ref;
     double conc_mult[5], hit_rate[5], knot[24];
+    /* Page-Hinkley exploitation switch (ENV.md §4.10; Eq. 2) */
+    uint32_t ph_enable, ph_window;     /* on/off; quiet window W (50) */
+    double ph_delta, ph_lambda;        /* δ (0.005), λ (50·δ) */
 } orc_config;
 
 typedef struct {                       /* per-tuner hyper-parameters (the sweep axes) */
@@ -55,7 +58,14 @@ typedef struct {                       /* ENV.md §4.9 */
              near_tie_steps, follow_violations;
     double sum_energy, sum_tpot, sum_ttft, sum_edp, sum_reward, base_energy, base_edp;
     double max_viol_rel;               /* follow mode: worst (s_max - s_gpu)/scale seen */
+    /* ENV.md §4.10 */
+    uint32_t exploit_steps;            /* steps selected greedily (Eq. 2) */
+    uint32_t ph_alarms;                /* Page-Hinkley drift alarms */
+    uint32_t first_exploit_t;          /* first step t after which the phase became Exploitation (ORC_NEVER) */
+    uint32_t phase;                    /* final phase: 0 Exploration, 1 Exploitation */
 } orc_stats;
+
+#define ORC_NEVER 0xFFFFFFFFu
 
 typedef struct {                       /* final per-arm state, row-major */
     double A[ORC_MAX_ARMS][ORC_MAX_D][ORC_MAX_D];

@@ -37,6 +37,19 @@ FP64_UNITS_PER_SM = 64           # FP64 FMA lanes per SM (B200)
 N_SM = 148
 
 
+def profile_traffic():
+    """DRAM bytes (read + write) of all replay-class launches of one default bench step, from
+    the committed ncu capture (tools/gpu_traffic.sh → profiles/r01_v8_traffic.json), or None."""
+    path = os.path.join(ROOT, "profiles", "r01_v8_traffic.json")
+    try:
+        with open(path) as f:
+            tot = json.load(f)["_replay_total"]
+        return tot["dram_bytes"], ("ncu dram__bytes_read+write summed over the replay launches of one "
+                                   "C4 bench step (profiles/r01_v8_traffic.json)")
+    except (OSError, KeyError, ValueError):
+        return None, None
+
+
 def flops_per_step(d: int, k_act_sum: float, steps: float) -> float:
     """Algorithmic FP64 flops: per active arm d²+3d+3 (Eq. 1 score) + 5
     (pruning bookkeeping); per step 3d²+8d+4 (Sherman–Morrison + RLS update) + 50
@@ -123,6 +136,8 @@ def main():
     ap.add_argument("--T", type=int, default=None, help="override decision windows (debug only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--phase", action="store_true",
+                    help="enable the Page-Hinkley exploitation phase (ENV.md §4.10; not the §8(a) headline)")
     ap.add_argument("--policy", type=int, default=int(os.environ.get("AGFT_POLICY", "0")),
                     help="0 auto (SOLO/SEG/WIDE), 1 wide only, 2 SOLO/MSEG/WIDE")
     ap.add_argument("--scaling", default=None, choices=["weak", "strong"],
@@ -142,6 +157,8 @@ def main():
     cfg = named_config(args.config)
     if args.T:
         cfg["T"] = args.T
+    if args.phase:
+        cfg["ph_enable"] = 1          # ENV.md §4.10 exploitation phase
     T = cfg["T"]
 
     if args.impl == "reference":
@@ -210,10 +227,13 @@ def main():
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    from paper_2508_01744_b200 import _abi
+    launches0 = _abi.lib().agft_kernel_launches()
     start.record(stream)
     for _ in range(args.steps):
         one_step(True)
     end.record(stream)
+    launches = int(_abi.lib().agft_kernel_launches() - launches0)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -237,8 +257,11 @@ def main():
     pk = peaks()
     sm_mhz = float(pk.get("sm_max_mhz", 1965.0))
     peak_fp64 = N_SM * FP64_UNITS_PER_SM * 2 * sm_mhz * 1e6 / 1e12
+    traffic, traffic_src = profile_traffic()
     roofline = {"bound": "alu", "achieved": round(achieved, 4), "peak": round(peak_fp64, 2),
-                "unit": "TFLOP/s", "frac": round(achieved / peak_fp64, 5), "traffic": None,
+                "unit": "TFLOP/s", "frac": round(achieved / peak_fp64, 5), "traffic": traffic,
+                "traffic_scope": traffic_src,
+                "algorithmic_hbm_bytes_per_step": 128 * T * R + STATS_DTYPE.itemsize * n,   # records once + stats
                 "kernel": "replay_kernel", "replay_share": round(replay_ms / ms, 4),
                 "peak_source": "derived: 148 SM × 64 FP64 FMA/clk × 2 × sm_max_mhz (DESIGN.md §5)",
                 "mean_active_arms": round(sum_active / (float(n) * T), 3)}
@@ -249,11 +272,12 @@ def main():
            "config": {"workload": f"{args.config}: {n} tuners/GPU × {cfg['n_arms']} arms × d={cfg['d']} × "
                                   f"{T} windows ({R} traces/GPU, α×pruning sweep, diurnal+burst)",
                       "tuners_per_gpu": n, "T": T, "arms": cfg["n_arms"], "d": cfg["d"],
+                      "phase_switch": bool(cfg.get("ph_enable", 0)),
                       "traces_per_gpu": R, "chunk": chunk,
                       "l2": f"inputs larger than L2: tuner state {tb.workspace.numel() / 2**30:.2f} GiB/GPU",
                       "parallelism": f"tuner shards dp{world}"},
            "roofline": roofline, "clocks": clk,
-           "gpu_launches": args.steps * (2 + 2 * n_chunks), "all_steps_complete": steps_ok}
+           "gpu_launches": launches, "all_steps_complete": steps_ok}
 
     if not args.no_e2e:
         out["e2e"] = e2e_leg(cfg, params, sh.trace_base, world, local, chunk, n, T, args)
@@ -313,10 +337,13 @@ def sweep_bench(args, cfg, rank, world, local):
     clocks = ClockSampler(local)
     clocks.start()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    from paper_2508_01744_b200 import _abi
+    launches0 = _abi.lib().agft_kernel_launches()
     start.record(stream)
     for _ in range(args.steps):
         sums = one(True)
     end.record(stream)
+    launches = int(_abi.lib().agft_kernel_launches() - launches0)
     torch.cuda.synchronize()
     clk = clocks.stop()
     ms = start.elapsed_time(end)
@@ -343,7 +370,7 @@ def sweep_bench(args, cfg, rank, world, local):
                         "kernel": "sweep_kernel", "kernel_share": round(k_ms / ms, 4),
                         "flops_per_eval": SWEEP_FLOPS,
                         "peak_source": "derived: 148 SM × 64 FP64 FMA/clk × 2 × sm_max_mhz (DESIGN.md §5)"},
-           "clocks": clk, "gpu_launches": args.steps * (2 * ((T + chunk - 1) // chunk) + 2),
+           "clocks": clk, "gpu_launches": launches,
            "check": {"windows_counted": int(h["NP"].sum()) == R * T,
                      "oracle_le_fixed": bool(np.all(h["O"][:, 0][:, None] <= h["S"][:, :, 2]))}}
     if rank == 0:

@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define AGFT_ABI_VERSION 1u
+#define AGFT_ABI_VERSION 2u         /* 2: + agft_phase, + Page-Hinkley stats */
 #define AGFT_MAX_ARMS 128u          /* K ≤ 128 */
 #define AGFT_MAX_D 7u               /* the paper's 7-dim context */
 #define AGFT_MAX_WINDOW 64u         /* reward-median window, AMB-3 */
@@ -87,6 +87,12 @@ typedef struct {
     double conc_mult[5], hit_rate[5], knot[24];
 } agft_trace_cfg;
 
+/* Exploitation phase (Eq. 2; ENV.md §4.10): a classical Page-Hinkley detector on
+ * the reward stream.  enable = 0 is the §8(a) hot path.  When the
+ * tuner has seen `window` observations since the last alarm it selects greedily (α_t = 0,
+ * Eq. 2); an alarm (cum − min > lambda) resets the detector and re-enters Exploration. */
+typedef struct { uint32_t enable, window; double delta, lambda; } agft_phase;
+
 typedef struct {
     uint32_t abi_version;     /* must be AGFT_ABI_VERSION */
     uint32_t n_tuners;        /* N ≥ 1 */
@@ -103,6 +109,7 @@ typedef struct {
     agft_trace_cfg trace;
     double norm_lo[7], norm_hi[7];   /* context normalisation bounds (AMB-14) */
     uint64_t env_seed;               /* S in ENV.md §1 */
+    agft_phase phase;                /* Page-Hinkley exploitation switch (ENV.md §4.10) */
 } agft_config;
 
 /* Per-tuner parameters (the hyper-parameter sweep axes of C4/C5). */
@@ -114,14 +121,20 @@ typedef struct {
     double historical_k;      /* k_h, P:388 (1.0) */
 } agft_tuner_params;          /* 32 B */
 
-/* Per-tuner statistics (ENV.md §4.9), 104 B. */
+/* Per-tuner statistics (ENV.md §4.9, §4.10), 120 B. */
 typedef struct {
     uint64_t traj_hash;       /* FNV-1a over the chosen arm of every step */
     uint64_t sum_active;      /* Σ_t |F_available(t)| before pruning (work counter) */
     uint32_t steps, last_arm, n_active, n_pruned_extreme, n_pruned_hist, n_pruned_cascade,
              near_tie_steps, flags;
     double sum_energy, sum_tpot, sum_ttft, sum_edp, sum_reward, base_energy, base_edp;
+    uint32_t exploit_steps;   /* steps selected greedily (Eq. 2), §4.10 */
+    uint32_t ph_alarms;       /* Page-Hinkley drift alarms */
+    uint32_t first_exploit_t; /* first step after which the phase was Exploitation, AGFT_NEVER if none */
+    uint32_t phase;           /* current phase: 0 Exploration, 1 Exploitation */
 } agft_tuner_stats;
+
+#define AGFT_NEVER 0xFFFFFFFFu
 
 /* Host-only validation of a config (the checks agft_create makes before touching
  * the device): grid, dimensions, finiteness/ranges. */
@@ -212,6 +225,10 @@ agft_status agft_regret(agft_handle h, const double *d_S, const double *d_SP, co
 
 /* Frees the host handle only; the caller frees its device buffers. */
 agft_status agft_destroy(agft_handle h);
+
+/* Process-wide number of CUDA kernels this library has launched so far (host counter,
+ * incremented at every <<<>>> the library issues; never synchronises). */
+uint64_t agft_kernel_launches(void);
 
 const char *agft_status_string(agft_status s);
 

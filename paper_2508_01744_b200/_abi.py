@@ -14,7 +14,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("AGFT_LIB_PATH") or os.path.join(HERE, "libagft.so")   # override: A/B builds
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 RECORD_BYTES = 128
 ROW_WORDS = 12
 NO_RECORD = 0xFFFFFFFF
@@ -53,11 +53,16 @@ class AgftTraceCfg(C.Structure):
                 ("conc_mult", f64 * 5), ("hit_rate", f64 * 5), ("knot", f64 * 24)]
 
 
+class AgftPhase(C.Structure):
+    _fields_ = [("enable", u32), ("window", u32), ("delta", f64), ("lambda_", f64)]
+
+
 class AgftConfig(C.Structure):
     _fields_ = [("abi_version", u32), ("n_tuners", u32), ("d", u32), ("n_traces", u32),
                 ("trace_base", u32), ("record_slots", u32), ("kernel_policy", u32), ("pad0", u32),
                 ("grid", AgftGrid), ("prune", AgftPrune), ("policy", AgftPolicy), ("env", AgftEnv),
-                ("trace", AgftTraceCfg), ("norm_lo", f64 * 7), ("norm_hi", f64 * 7), ("env_seed", u64)]
+                ("trace", AgftTraceCfg), ("norm_lo", f64 * 7), ("norm_hi", f64 * 7), ("env_seed", u64),
+                ("phase", AgftPhase)]
 
 
 PARAMS_DTYPE = np.dtype([("trace_id", "<u4"), ("record_slot", "<u4"), ("alpha0", "<f8"),
@@ -68,8 +73,9 @@ STATS_DTYPE = np.dtype([("traj_hash", "<u8"), ("sum_active", "<u8"),
                         ("n_pruned_cascade", "<u4"), ("near_tie_steps", "<u4"), ("flags", "<u4"),
                         ("sum_energy", "<f8"), ("sum_tpot", "<f8"), ("sum_ttft", "<f8"),
                         ("sum_edp", "<f8"), ("sum_reward", "<f8"), ("base_energy", "<f8"),
-                        ("base_edp", "<f8")])
-assert PARAMS_DTYPE.itemsize == 32 and STATS_DTYPE.itemsize == 104
+                        ("base_edp", "<f8"), ("exploit_steps", "<u4"), ("ph_alarms", "<u4"),
+                        ("first_exploit_t", "<u4"), ("phase", "<u4")])
+assert PARAMS_DTYPE.itemsize == 32 and STATS_DTYPE.itemsize == 120
 
 STATUS = {0: "ok", -1: "invalid argument", -2: "invalid frequency grid", -3: "empty arm set",
           -4: "context dimension out of range", -5: "non-finite or out-of-range coefficient",
@@ -95,6 +101,7 @@ PROTOTYPES = {
     "agft_regret": (C.c_int, [vp, vp, vp, vp, vp, vp, vp]),
     "agft_destroy": (C.c_int, [vp]),
     "agft_status_string": (C.c_char_p, [C.c_int]),
+    "agft_kernel_launches": (C.c_uint64, []),
 }
 
 _lib = None
@@ -162,6 +169,8 @@ def make_config(cfg: dict, n_tuners: int | None = None, n_traces: int | None = N
         c.norm_lo[i] = cfg["norm_lo"][i]
         c.norm_hi[i] = cfg["norm_hi"][i]
     c.env_seed = cfg["seed"]
+    c.phase = AgftPhase(cfg.get("ph_enable", 0), cfg.get("ph_window", 50), cfg.get("ph_delta", 0.005),
+                        cfg.get("ph_lambda", 0.25))
     return c
 
 

@@ -4,6 +4,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <new>
 
 #include "agft_internal.cuh"
@@ -21,6 +22,11 @@ struct agft_handle_s {
     uint32_t sweep_t;       // next window of the offline sweep (ENV.md §5 accumulation order)
     agft_status sticky;     // AGFT_OK or AGFT_E_CUDA
 };
+
+namespace agft {
+static std::atomic<uint64_t> g_launches{0};
+void note_launches(uint32_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+}  // namespace agft
 
 namespace {
 
@@ -45,6 +51,12 @@ int mseg_g()
         return (v == 1 || v == 2 || v == 4 || v == 8) ? v : 4;
     }();
     return g;
+}
+
+bool stream_prio_enabled()
+{
+    const char *e = std::getenv("AGFT_STREAM_PRIO");
+    return e && e[0] == '1';
 }
 
 // AGFT_LANE_EXACT=1: LANE evaluates the canonical pruning tree every window (tests, A/B)
@@ -81,6 +93,10 @@ agft_status validate(const agft_config *c)
         !finite(p.tie_rel) || p.tie_rel < 0)
         return AGFT_E_NONFINITE;
     if (p.median_window < 1 || p.median_window > AGFT_MAX_WINDOW) return AGFT_E_INVALID_ARG;
+    const agft_phase &ph = c->phase;                 // ENV.md §4.10
+    if (ph.enable > 1u) return AGFT_E_INVALID_ARG;
+    if (ph.enable && (ph.window < 1u || !finite(ph.delta) || !finite(ph.lambda) || ph.delta < 0 || ph.lambda < 0))
+        return ph.window < 1u ? AGFT_E_INVALID_ARG : AGFT_E_NONFINITE;
     const agft_env &e = c->env;
     const double ev[] = {e.window_s, e.p_idle, e.k_lin, e.k_cube, e.u_floor, e.u_max, e.c_prefill,
                          e.c_decode, e.beta, e.sigma_e, e.sigma_t};
@@ -146,6 +162,10 @@ ReplayArgs replay_args(agft_handle h, const void *records, uint32_t t0, uint32_t
     a.clip_lo = c.policy.clip_lo;
     a.clip_hi = c.policy.clip_hi;
     a.tie_rel = c.policy.tie_rel;
+    a.ph_enable = c.phase.enable;
+    a.ph_window = c.phase.window;
+    a.ph_delta = c.phase.delta;
+    a.ph_lambda = c.phase.lambda;
     // ENV.md §4.8: (double)F_k < cascade_fraction * (double)f_max_hw — one IEEE product
     volatile double cf = c.prune.cascade_fraction;
     a.cascade_limit = cf * (double)c.grid.f_max_hw_mhz;
@@ -211,8 +231,18 @@ agft_status agft_create(const agft_config *cfg, const agft_tuner_params *d_param
     }
 
     cudaError_t e = cudaEventCreateWithFlags(&h->fork, cudaEventDisableTiming);
+    // Class streams by priority (AGFT_STREAM_PRIO=1): the multi-wave SEG classes first, so the
+    // block scheduler fills SMs longest-work-first and the short classes pack around them.
+    int prio_lo = 0, prio_hi = 0;
+    const bool prio = stream_prio_enabled() && cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi) == cudaSuccess;
     for (int c = 0; c < kNumCls && e == cudaSuccess; ++c) {
-        e = cudaStreamCreateWithFlags(&h->side[c], cudaStreamNonBlocking);
+        int p = prio_lo;
+        if (prio) {
+            // rank: SEG16 (9..16 arms) > SEG32 (17..32) > SEG8 (2..8) > SEG64 / WIDE > SOLO
+            const int rank = c == kClsSeg16 ? 0 : c == kClsSeg32 ? 1 : c == kClsSeg8 ? 2 : c == kClsSolo ? 4 : 3;
+            p = prio_hi + rank * (prio_lo - prio_hi) / 4;
+        }
+        e = cudaStreamCreateWithPriority(&h->side[c], cudaStreamNonBlocking, p);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->join[c], cudaEventDisableTiming);
     }
     if (e == cudaSuccess)
@@ -285,8 +315,9 @@ static agft_status run_steps(agft_handle h, const void *d_records, uint32_t t0, 
         if (c.kernel_policy == AGFT_POLICY_WIDE) {
             e = launch_replay(a, c.d, h->stream);
         } else {
-            const bool split = c.kernel_policy != AGFT_POLICY_MSEG;
-            const bool lane = c.kernel_policy == AGFT_POLICY_LANE && lane_supported(c.d);
+            // MSEG and LANE do not implement the exploitation phase (ENV.md §4.10): AUTO instead
+            const bool split = c.kernel_policy != AGFT_POLICY_MSEG || c.phase.enable;
+            const bool lane = c.kernel_policy == AGFT_POLICY_LANE && lane_supported(c.d) && !c.phase.enable;
             a.force_exact = lane_force_exact();
             e = launch_classify(h->ws, c.n_tuners, split, h->stream);
             if (e == cudaSuccess) e = cudaEventRecord(h->fork, h->stream);
@@ -420,6 +451,8 @@ agft_status agft_destroy(agft_handle h)
     delete h;
     return AGFT_OK;
 }
+
+uint64_t agft_kernel_launches(void) { return agft::g_launches.load(std::memory_order_relaxed); }
 
 const char *agft_status_string(agft_status s)
 {

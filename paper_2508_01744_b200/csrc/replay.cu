@@ -109,6 +109,13 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
     const uint64_t tb = a.list ? a.list[widx] : widx;
     agft_tuner_stats st = a.w.acc[tb];
     if (st.flags & 1u) return;                        // frozen by an earlier anomaly
+    __shared__ PhState s_ph[kWarpsPerBlock];          // ENV.md §4.10 detector (lane 0 owns it)
+    uint32_t phase = 0u;
+    if (a.ph_enable) {
+        if (lane == 0) s_ph[warp] = a.w.ph[tb];
+        __syncwarp();
+        phase = s_ph[warp].phase;
+    }
 
     double *sA = smem + 3 * kMaxArms + (size_t)warp * S * (P + D) * 32;
     double *sT = sA + S * P * 32;
@@ -154,7 +161,7 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
         for (int j = 0; j < S; ++j) nact += popc_ballot((act >> j) & 1u);
 
         // ---- a3: α_t = α0/√(1+t/τ)
-        const double alpha = alpha_t(prm.alpha0, t, 1.0 / a.tau);
+        const double alpha = phase ? 0.0 : alpha_t(prm.alpha0, t, 1.0 / a.tau);   // Exploitation: Eq. 2
 
         // ---- a4: Eq. 1 scores.  q = Σ_{i≤j} w_ij A⁻¹_ij with w_ij = x_i x_j (×2 off-diagonal)
         double w[P];
@@ -240,6 +247,14 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
         if (!isfinite(edp) || !isfinite(r)) {         // anomaly: flag and freeze the tuner
             st.flags |= 1u;
             break;
+        }
+        if (a.ph_enable) {                            // ENV.md §4.10 observe_reward
+            if (lane == 0) {
+                s_ph[warp].exploit_steps += phase;
+                ph_observe(s_ph[warp], r, t, a.ph_window, a.ph_delta, a.ph_lambda);
+            }
+            __syncwarp();
+            phase = s_ph[warp].phase;
         }
         uint32_t ri;
         if (wcount < M) {
@@ -449,6 +464,10 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
         a.w.wmeta[tb * 2] = wcount;
         a.w.wmeta[tb * 2 + 1] = whead;
         st.n_active = (uint32_t)nact_end;
+        if (a.ph_enable) {
+            a.w.ph[tb] = s_ph[warp];
+            ph_to_stats(s_ph[warp], st);
+        }
         a.w.acc[tb] = st;
     }
 }
@@ -462,7 +481,7 @@ static cudaError_t launch_ds(const ReplayArgs &a, cudaStream_t s)
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const uint32_t blocks = (a.n_tuners + kWarpsPerBlock - 1) / kWarpsPerBlock;
-    kern<<<blocks, kWarpsPerBlock * 32, smem, s>>>(a);
+    kern<<<blocks, kWarpsPerBlock * 32, smem, s>>>(a); note_launches(1);
     return cudaGetLastError();
 }
 

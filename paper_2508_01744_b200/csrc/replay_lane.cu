@@ -530,7 +530,7 @@ static cudaError_t launch_lane_dk(const ReplayArgs &a, cudaStream_t s)
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const uint32_t blocks = (a.n_tuners + 31) / 32;
-    kern<<<blocks, 32, smem, s>>>(a);
+    kern<<<blocks, 32, smem, s>>>(a); note_launches(1);
     return cudaGetLastError();
 }
 

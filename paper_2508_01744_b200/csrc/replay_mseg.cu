@@ -451,7 +451,7 @@ static cudaError_t launch_mseg_dg(const ReplayArgs &a, cudaStream_t s)
 {
     constexpr int per_block = kMsegTunersPerBlock;
     const uint32_t blocks = (a.n_tuners + per_block - 1) / per_block;
-    mseg_kernel<D, G><<<blocks, kMsegTunersPerBlock * G, 0, s>>>(a);
+    mseg_kernel<D, G><<<blocks, kMsegTunersPerBlock * G, 0, s>>>(a); note_launches(1);
     return cudaGetLastError();
 }
 

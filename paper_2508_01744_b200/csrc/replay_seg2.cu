@@ -162,6 +162,14 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
     if (l == 0) st = a.w.acc[tb];
     __syncwarp();
     bool live = valid && !(st.flags & 1u);
+    __shared__ PhState s_ph[kSeg2Warps * (32 / G)];   // ENV.md §4.10 detector (lane 0 of the segment)
+    PhState &ph = s_ph[warp * NSEG + sg];
+    uint32_t phase = 0u;
+    if (a.ph_enable) {
+        if (l == 0) ph = a.w.ph[tb];
+        __syncwarp();
+        phase = ph.phase;
+    }
     const agft_tuner_params prm = a.w.params[tb];
 
     // ---- compact the active arms: lane l ← active-order arms l and G + l
@@ -226,7 +234,7 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
         double x[D];
 #pragma unroll
         for (int i = 0; i < D; ++i) x[i] = __ldg(&rc->x[i]);
-        const double alpha = alpha_t(prm.alpha0, t, inv_tau);
+        const double alpha = phase ? 0.0 : alpha_t(prm.alpha0, t, inv_tau);   // Exploitation: Eq. 2
 
         // ---- a4: both slots
         double w[P];
@@ -305,6 +313,14 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
         if (!isfinite(o.edp) || !isfinite(r)) {
             if (live && l == 0) st.flags |= 1u;
             live = false;
+        }
+        if (a.ph_enable) {                                            // ENV.md §4.10 observe_reward
+            if (live && l == 0) {
+                ph.exploit_steps += phase;
+                ph_observe(ph, r, t, a.ph_window, a.ph_delta, a.ph_lambda);
+            }
+            __syncwarp();
+            phase = ph.phase;
         }
         if (wcount < M) {
             winsert<G, E>(S, o.edp, wless<G, E>(S, o.edp), l);
@@ -444,6 +460,10 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
         a.w.wmeta[(size_t)tb * 2] = wcount;
         a.w.wmeta[(size_t)tb * 2 + 1] = whead;
         st.n_active = (uint32_t)nact;
+        if (a.ph_enable) {
+            a.w.ph[tb] = ph;
+            ph_to_stats(ph, st);
+        }
         a.w.acc[tb] = st;
     }
 }
@@ -458,7 +478,7 @@ static cudaError_t launch_seg2_dg(const ReplayArgs &a, cudaStream_t s)
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const uint32_t blocks = (a.n_tuners + per_block - 1) / per_block;
-    kern<<<blocks, kSeg2Warps * 32, smem, s>>>(a);
+    kern<<<blocks, kSeg2Warps * 32, smem, s>>>(a); note_launches(1);
     return cudaGetLastError();
 }
 

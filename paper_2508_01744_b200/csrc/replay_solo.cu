@@ -35,6 +35,9 @@ __global__ void __launch_bounds__(kSoloThreads, kSoloMinBlocks) solo_kernel(cons
 
     agft_tuner_stats st = a.w.acc[tb];
     if (st.flags & 1u) return;
+    __shared__ PhState s_ph[kSoloThreads];                       // ENV.md §4.10 detector of this lane
+    PhState &ph = s_ph[threadIdx.x];
+    if (a.ph_enable) ph = a.w.ph[tb];
     const agft_tuner_params prm = a.w.params[tb];
     int k = 0;
     {
@@ -75,6 +78,10 @@ __global__ void __launch_bounds__(kSoloThreads, kSoloMinBlocks) solo_kernel(cons
             st.flags |= 1u;
             break;
         }
+        if (a.ph_enable) {                                       // ENV.md §4.10 (one arm: α is moot)
+            ph.exploit_steps += ph.phase;
+            ph_observe(ph, r, a.t0 + s, a.ph_window, a.ph_delta, a.ph_lambda);
+        }
         // a9: Eqs. 3–5 on the (only) chosen arm, Welford means
         double x[D];
 #pragma unroll
@@ -104,6 +111,10 @@ __global__ void __launch_bounds__(kSoloThreads, kSoloMinBlocks) solo_kernel(cons
     a.w.wmeta[(size_t)tb * 2] = wcount;
     a.w.wmeta[(size_t)tb * 2 + 1] = whead;
     st.n_active = 1;
+    if (a.ph_enable) {
+        a.w.ph[tb] = ph;
+        ph_to_stats(ph, st);
+    }
     a.w.acc[tb] = st;
 #undef SW
 }
@@ -112,7 +123,7 @@ template <int D>
 static cudaError_t launch_solo_d(const ReplayArgs &a, cudaStream_t s)
 {
     const uint32_t blocks = (a.n_tuners + kSoloThreads - 1) / kSoloThreads;
-    solo_kernel<D><<<blocks, kSoloThreads, 0, s>>>(a);
+    solo_kernel<D><<<blocks, kSoloThreads, 0, s>>>(a); note_launches(1);
     return cudaGetLastError();
 }
 

@@ -82,9 +82,9 @@ __global__ void __launch_bounds__(kPartBlock) class_scatter_kernel(Ws w, uint32_
 cudaError_t launch_classify(const Ws &w, uint32_t N, bool split, cudaStream_t s)
 {
     const uint32_t nblk = (N + kPartBlock - 1) / kPartBlock;
-    class_count_kernel<<<nblk, kPartBlock, 0, s>>>(w, N, split);
-    class_scan_kernel<<<1, 32, 0, s>>>(w, nblk);
-    class_scatter_kernel<<<nblk, kPartBlock, 0, s>>>(w, N, split);
+    class_count_kernel<<<nblk, kPartBlock, 0, s>>>(w, N, split); note_launches(1);
+    class_scan_kernel<<<1, 32, 0, s>>>(w, nblk); note_launches(1);
+    class_scatter_kernel<<<nblk, kPartBlock, 0, s>>>(w, N, split); note_launches(1);
     return cudaGetLastError();
 }
 

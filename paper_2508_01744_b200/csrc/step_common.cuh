@@ -49,6 +49,37 @@ __device__ __forceinline__ void welford(uint32_t &n, double &rbar, double &ebar,
     ebar = xadd(ebar, xmul(xsub(edp, ebar), inv));
 }
 
+// ENV.md §4.10 observe_reward: the Page-Hinkley detector on the reward of step t (after a8)
+__device__ __forceinline__ void ph_observe(PhState &p, double r, uint32_t t, uint32_t W, double delta, double lambda)
+{
+    p.n += 1u;
+    const double inv = xdiv(1.0, (double)p.n);
+    p.mean = xadd(p.mean, xmul(xsub(r, p.mean), inv));
+    p.cum = xadd(p.cum, xsub(xsub(r, p.mean), delta));
+    if (p.cum < p.min) p.min = p.cum;
+    p.quiet += 1u;
+    if (xsub(p.cum, p.min) > lambda) {               // drift alarm: reset, re-enter Exploration
+        p.alarms += 1u;
+        p.quiet = 0u;
+        p.n = 0u;
+        p.mean = 0.0;
+        p.cum = 0.0;
+        p.min = 0.0;
+        p.phase = 0u;
+    } else if (p.phase == 0u && p.quiet >= W) {       // W quiet observations: Exploitation (Eq. 2)
+        p.phase = 1u;
+        if (p.first_exploit_t == AGFT_NEVER) p.first_exploit_t = t;
+    }
+}
+
+__device__ __forceinline__ void ph_to_stats(const PhState &p, agft_tuner_stats &st)
+{
+    st.exploit_steps = p.exploit_steps;
+    st.ph_alarms = p.alarms;
+    st.first_exploit_t = p.first_exploit_t;
+    st.phase = p.phase;
+}
+
 // a11: stats in ENV.md §4.9 order
 __device__ __forceinline__ void stats_add(agft_tuner_stats &st, const Response &o, double r, double baseE,
                                           double baseEDP, int kstar, uint32_t nact)

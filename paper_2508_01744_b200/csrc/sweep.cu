@@ -236,7 +236,7 @@ cudaError_t launch_sweep(const Ws &w, const agft_config &c, const void *records,
     a.p_idle = c.env.p_idle;
     a.u_floor = c.env.u_floor;
     a.u_max = c.env.u_max;
-    sweep_kernel<<<c.n_traces, kThreads, 0, s>>>(a);
+    sweep_kernel<<<c.n_traces, kThreads, 0, s>>>(a); note_launches(1);
     return cudaGetLastError();
 }
 
@@ -244,8 +244,11 @@ cudaError_t launch_regret(const Ws &w, const agft_config &c, const double *S, co
                           const double *O, uint8_t *koff, double *regret, cudaStream_t s)
 {
     const uint32_t nk = c.n_traces * 6u;
-    offline_kernel<<<(nk + 127) / 128, 128, 0, s>>>(S, SP, NP, c.n_traces, c.grid.n_arms, koff);
-    if (regret) regret_kernel<<<(c.n_tuners + 255) / 256, 256, 0, s>>>(w, c.n_tuners, c.grid.n_arms, S, O, koff, regret);
+    offline_kernel<<<(nk + 127) / 128, 128, 0, s>>>(S, SP, NP, c.n_traces, c.grid.n_arms, koff); note_launches(1);
+    if (regret) {
+        regret_kernel<<<(c.n_tuners + 255) / 256, 256, 0, s>>>(w, c.n_tuners, c.grid.n_arms, S, O, koff, regret);
+        note_launches(1);
+    }
     return cudaGetLastError();
 }
 

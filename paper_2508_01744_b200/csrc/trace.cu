@@ -110,7 +110,7 @@ cudaError_t launch_trace(const TraceArgs &a, cudaStream_t s)
     const uint64_t n = (uint64_t)a.n_traces * a.n_steps;
     if (n == 0) return cudaSuccess;
     const uint32_t blocks = (uint32_t)((n + 255) / 256);
-    trace_kernel<<<blocks, 256, 0, s>>>(a);
+    trace_kernel<<<blocks, 256, 0, s>>>(a); note_launches(1);
     return cudaGetLastError();
 }
 
@@ -184,7 +184,11 @@ __global__ void init_tuner_kernel(const __grid_constant__ InitArgs a)
             agft_tuner_stats st = {};
             st.traj_hash = kFnvOffset;
             st.n_active = a.K;
+            st.first_exploit_t = AGFT_NEVER;
             a.w.acc[tb] = st;
+            PhState ph = {};
+            ph.first_exploit_t = AGFT_NEVER;
+            a.w.ph[tb] = ph;
         }
     }
 }
@@ -200,11 +204,11 @@ cudaError_t launch_init(const Ws &w, const agft_config &cfg, cudaStream_t s)
     a.f_step_mhz = cfg.grid.f_step_mhz;
     a.f_max_hw_mhz = cfg.grid.f_max_hw_mhz;
     a.env = cfg.env;
-    init_env_kernel<<<1, kMaxArms, 0, s>>>(a);
+    init_env_kernel<<<1, kMaxArms, 0, s>>>(a); note_launches(1);
     const uint64_t total = (uint64_t)a.N * kMaxArms;
     uint32_t blocks = (uint32_t)((total + 255) / 256);
     if (blocks > 148u * 32u) blocks = 148u * 32u;
-    init_tuner_kernel<<<blocks, 256, 0, s>>>(a);
+    init_tuner_kernel<<<blocks, 256, 0, s>>>(a); note_launches(1);
     return cudaGetLastError();
 }
 
@@ -233,7 +237,7 @@ cudaError_t launch_export(const Ws &w, uint32_t tuner, uint32_t K, uint32_t D, d
                           double *theta, uint32_t *n, double *rbar, double *ebar, uint32_t *mask,
                           cudaStream_t s)
 {
-    export_kernel<<<1, kMaxArms, 0, s>>>(w, tuner, K, D, ainv, b, theta, n, rbar, ebar, mask);
+    export_kernel<<<1, kMaxArms, 0, s>>>(w, tuner, K, D, ainv, b, theta, n, rbar, ebar, mask); note_launches(1);
     return cudaGetLastError();
 }
 

@@ -45,7 +45,7 @@ def test_library_exports_every_declared_symbol(lib):
 def test_struct_mirrors_match(lib):
     assert lib.agft_struct_size(0) == __import__("ctypes").sizeof(_abi.AgftConfig)
     assert lib.agft_struct_size(1) == 32
-    assert lib.agft_struct_size(2) == 104
+    assert lib.agft_struct_size(2) == 120
 
 
 @pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5"])
@@ -76,7 +76,7 @@ def test_validation_codes(lib):
     c = _abi.make_config(named_config("C2"))
     c.abi_version = 99
     assert lib.agft_validate(c) == -1
-    c.abi_version = 1
+    c.abi_version = _abi.ABI_VERSION
     c.n_tuners = 0
     assert pkg.agft_workspace_bytes(c) == 0
 

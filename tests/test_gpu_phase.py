@@ -1,0 +1,64 @@
+"""GPU parity of the exploitation phase (ENV.md §4.10: Page-Hinkley detector, Eq. 2 greedy
+selection) against the oracle, through the C-ABI, on every schedule that implements it."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from agft_inputs import named_config, tuner_params  # noqa: E402
+
+from test_gpu_parity import _check, _run  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _device():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+
+
+def _cfg(name, **kw):
+    c = named_config(name)
+    c.update(ph_enable=1)
+    c.update(kw)
+    return c
+
+
+@pytest.mark.parametrize("policy", [0, 1, 3])
+def test_c2_phase_parity(policy):
+    cfg = _cfg("C2")
+    tb, params, st, traj, _ = _run(cfg, 4500, record=[0], policy=policy)
+    _check(cfg, tb, params, st, [0], 4500, traj)
+    assert st["first_exploit_t"][0] != 0xFFFFFFFF and st["exploit_steps"][0] > 0
+
+
+@pytest.mark.parametrize("kw", [
+    dict(ph_window=1, ph_lambda=1e300),              # greedy (Eq. 2) from step 1 on
+    dict(ph_window=5, ph_lambda=0.05),               # frequent alarms and re-entries
+    dict(ph_window=20, ph_delta=0.0),
+    dict(ph_window=3, hist_min_round=0, hist_min_samples=1),
+    dict(ph_window=10, n_arms=33, f_step_mhz=45, prune_enable=0),
+])
+@pytest.mark.parametrize("policy", [0, 1])
+def test_phase_edge_configs(kw, policy):
+    cfg = _cfg("C2", n_tuners=5, n_traces=5, T=900)
+    cfg.update(kw)
+    ids = list(range(5))
+    params = tuner_params(cfg, ids)
+    params["alpha0"] = np.array([0.0, 0.3, 1.0, 2.0, 5.0])
+    tb, params, st, traj, _ = _run(cfg, 900, params=params, record=ids, chunk=256, policy=policy)
+    _check(cfg, tb, params, st, ids, 900, traj)
+
+
+def test_c4_sweep_with_phase_sampled():
+    """One C4 trace's 256 hyper-parameter points with the phase switch on, 20,000 windows, in
+    the bench's launch configuration (all kernel classes, SOLO included)."""
+    cfg = _cfg("C4", n_traces=1)
+    ids = list(range(256))
+    params = tuner_params(cfg, ids)
+    sample = [0, 15, 48, 63, 100, 200, 255]
+    tb, params, st, traj, _ = _run(cfg, 20000, params=params, record=sample, chunk=4500)
+    _check(cfg, tb, params, st, sample, 20000, traj)
+    assert np.all(st["steps"] == 20000) and np.all(st["flags"] == 0)
+    assert (st["exploit_steps"] > 0).mean() > 0.5

@@ -136,6 +136,7 @@ def main():
     ap.add_argument("--T", type=int, default=None, help="override decision windows (debug only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--chunk", type=int, default=CHUNK, help="windows per agft_replay call (records buffer)")
     ap.add_argument("--phase", action="store_true",
                     help="enable the Page-Hinkley exploitation phase (ENV.md §4.10; not the §8(a) headline)")
     ap.add_argument("--policy", type=int, default=int(os.environ.get("AGFT_POLICY", "0")),
@@ -188,7 +189,7 @@ def main():
     params = sh.params                                # local trace ids 0..R-1
     tb = TunerBatch(cfg, params, device=f"cuda:{local}", trace_base=sh.trace_base, policy=args.policy)
     stream = torch.cuda.current_stream()
-    chunk = min(CHUNK, T)
+    chunk = min(args.chunk, T)
     records = tb.new_records(chunk)
     stats_out = tb.stats_tensor()
     coll_dev = stats_out.device if args.backend == "nccl" else torch.device("cpu")

@@ -35,11 +35,20 @@ bool finite(double v) { return std::isfinite(v); }
 // Sub-chunk length between re-classifications: short while the action spaces are still
 // collapsing (most tuners reach K_act ≤ 32 within ~1,000 windows and K_act = 1 within
 // ~1,400), long once the classes are stable.
+uint32_t env_u32(const char *name, uint32_t def)
+{
+    const char *e = std::getenv(name);
+    const long v = e ? std::atol(e) : 0;
+    return v > 0 ? (uint32_t)v : def;
+}
+
 uint32_t sub_chunk(uint32_t t)
 {
-    if (t < 2048) return 256;
-    if (t < 8192) return 1024;
-    return 4096;
+    static const uint32_t early = env_u32("AGFT_SUB_EARLY", 256), mid = env_u32("AGFT_SUB_MID", 1024),
+                          late = env_u32("AGFT_SUB_LATE", 4096);
+    if (t < 2048) return early;
+    if (t < 8192) return mid;
+    return late;
 }
 
 // lanes per tuner of the MSEG class (AGFT_MSEG_G ∈ {1, 2, 4, 8}; default 4)
@@ -56,7 +65,27 @@ int mseg_g()
 bool stream_prio_enabled()
 {
     const char *e = std::getenv("AGFT_STREAM_PRIO");
-    return e && e[0] == '1';
+    return !(e && e[0] == '0');
+}
+
+// rank[c] = position of class c in the priority order (0 = highest)
+void prio_order(int (&rank)[kNumCls])
+{
+    static const int def[kNumCls] = {kClsSeg16, kClsSeg32, kClsSeg8, kClsWide, kClsSeg64, kClsSolo};
+    int order[kNumCls];
+    for (int i = 0; i < kNumCls; ++i) order[i] = def[i];
+    if (const char *e = std::getenv("AGFT_PRIO_ORDER")) {
+        int n = 0, v = 0;
+        bool any = false;
+        for (const char *q = e;; ++q) {
+            if (*q >= '0' && *q <= '9') { v = v * 10 + (*q - '0'); any = true; continue; }
+            if (any && n < kNumCls && v < kNumCls) order[n++] = v;
+            v = 0; any = false;
+            if (!*q) break;
+        }
+    }
+    for (int c = 0; c < kNumCls; ++c) rank[c] = kNumCls - 1;
+    for (int i = kNumCls - 1; i >= 0; --i) rank[order[i]] = i;
 }
 
 // AGFT_LANE_EXACT=1: LANE evaluates the canonical pruning tree every window (tests, A/B)
@@ -231,16 +260,19 @@ agft_status agft_create(const agft_config *cfg, const agft_tuner_params *d_param
     }
 
     cudaError_t e = cudaEventCreateWithFlags(&h->fork, cudaEventDisableTiming);
-    // Class streams by priority (AGFT_STREAM_PRIO=1): the multi-wave SEG classes first, so the
-    // block scheduler fills SMs longest-work-first and the short classes pack around them.
+    // Class streams by priority: the multi-wave SEG classes first, so the block scheduler fills
+    // SMs longest-work-first and the short classes pack around them (A/B: −2.3% per C4 day,
+    // DESIGN.md §4).  AGFT_STREAM_PRIO=0 disables; AGFT_PRIO_ORDER="2,1,3,0,5,4" overrides the
+    // order (class ids of agft_internal.cuh, highest priority first).
     int prio_lo = 0, prio_hi = 0;
     const bool prio = stream_prio_enabled() && cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi) == cudaSuccess;
+    int rank[kNumCls];
+    prio_order(rank);
     for (int c = 0; c < kNumCls && e == cudaSuccess; ++c) {
         int p = prio_lo;
         if (prio) {
-            // rank: SEG16 (9..16 arms) > SEG32 (17..32) > SEG8 (2..8) > SEG64 / WIDE > SOLO
-            const int rank = c == kClsSeg16 ? 0 : c == kClsSeg32 ? 1 : c == kClsSeg8 ? 2 : c == kClsSolo ? 4 : 3;
-            p = prio_hi + rank * (prio_lo - prio_hi) / 4;
+            p = prio_hi + rank[c];
+            if (p > prio_lo) p = prio_lo;
         }
         e = cudaStreamCreateWithPriority(&h->side[c], cudaStreamNonBlocking, p);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->join[c], cudaEventDisableTiming);

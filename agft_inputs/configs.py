@@ -43,6 +43,9 @@ _BASE = {
     "tie_rel": 1e-9,
     # Page-Hinkley exploitation switch (ENV.md §4.10): off in C1–C5 (the §8(a) hot path)
     "ph_enable": 0, "ph_window": 50, "ph_delta": 0.005, "ph_lambda": 0.25,
+    # mixed maturity-based refinement (ENV.md §4.11): off in C1–C5
+    "rf_enable": 0, "rf_period": 25, "rf_mature": 100, "rf_min_samples": 4, "rf_half_mhz": 150,
+    "rf_step_mhz": 15,
     # pruning
     "prune_enable": 1, "ext_round_limit": 60, "ext_min_samples": 3, "ext_reward_threshold": -1.2,
     "hist_min_round": 30, "hist_min_samples": 6, "hist_k": 1.0, "cascade_fraction": 0.5,

@@ -50,6 +50,8 @@ class OrcConfig(C.Structure):
         ("tau_ref", f64),
         ("conc_mult", f64 * 5), ("hit_rate", f64 * 5), ("knot", f64 * 24),
         ("ph_enable", u32), ("ph_window", u32), ("ph_delta", f64), ("ph_lambda", f64),
+        ("rf_enable", u32), ("rf_period", u32), ("rf_mature", u32), ("rf_min_samples", u32),
+        ("rf_half_mhz", u32), ("rf_step_mhz", u32),
     ]
 
 
@@ -65,7 +67,8 @@ class OrcStats(C.Structure):
                 ("follow_violations", u32),
                 ("sum_energy", f64), ("sum_tpot", f64), ("sum_ttft", f64), ("sum_edp", f64),
                 ("sum_reward", f64), ("base_energy", f64), ("base_edp", f64), ("max_viol_rel", f64),
-                ("exploit_steps", u32), ("ph_alarms", u32), ("first_exploit_t", u32), ("phase", u32)]
+                ("exploit_steps", u32), ("ph_alarms", u32), ("first_exploit_t", u32), ("phase", u32),
+                ("n_refine", u32), ("last_anchor", u32)]
 
 
 MAXK, MAXD = 128, 7
@@ -134,6 +137,11 @@ def lib():
                                 C.POINTER(u32), C.POINTER(f64), C.POINTER(C.c_uint8)]
         L.orc_argmin.argtypes = [C.POINTER(f64), u32, u32]
         L.orc_argmin.restype = u32
+        L.orc_stat_anchor.argtypes = [C.POINTER(OrcConfig), C.POINTER(u32), C.POINTER(f64),
+                                      C.POINTER(C.c_uint8)]
+        L.orc_stat_anchor.restype = u32
+        L.orc_refine_window.argtypes = [C.POINTER(OrcConfig), u32, C.POINTER(C.c_uint8), C.POINTER(C.c_uint8)]
+        L.orc_refine_window.restype = u32
         L.orc_sizeof.argtypes = [C.c_int]
         L.orc_sizeof.restype = u32
         for i, s in enumerate([OrcConfig, OrcTuner, OrcStats, OrcArms, OrcStepRec, OrcRecord,
@@ -160,6 +168,25 @@ def make_config(cfg: dict) -> OrcConfig:
         else:
             setattr(oc, name, v)
     return oc
+
+
+def stat_anchor(cfg: dict, n, ebar, extreme=None):
+    """ENV.md §4.11 statistical anchor (arm index, or None)."""
+    K = cfg["n_arms"]
+    n = np.ascontiguousarray(n, dtype=np.uint32)
+    e = np.ascontiguousarray(ebar, dtype=np.float64)
+    x = np.zeros(K, np.uint8) if extreme is None else np.ascontiguousarray(extreme, dtype=np.uint8)
+    a = lib().orc_stat_anchor(C.byref(make_config(cfg)), _ptr(n, u32), _ptr(e, f64), _ptr(x, C.c_uint8))
+    return None if a == 0xFFFFFFFF else int(a)
+
+
+def refine_window(cfg: dict, anchor: int, extreme=None) -> np.ndarray:
+    """ENV.md §4.11 refined action space around arm `anchor` (uint8 mask [K])."""
+    K = cfg["n_arms"]
+    x = np.zeros(K, np.uint8) if extreme is None else np.ascontiguousarray(extreme, dtype=np.uint8)
+    out = np.zeros(K, np.uint8)
+    lib().orc_refine_window(C.byref(make_config(cfg)), anchor, _ptr(x, C.c_uint8), _ptr(out, C.c_uint8))
+    return out
 
 
 def make_tuner(trace_id=0, alpha0=1.0, ext_reward_threshold=-1.2, hist_k=1.0) -> OrcTuner:

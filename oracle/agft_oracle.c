@@ -382,7 +382,36 @@ typedef struct {
     /* Page-Hinkley detector (ENV.md §4.10) */
     uint32_t phase, ph_quiet, ph_n;
     double ph_mean, ph_cum, ph_min;
+    uint8_t extreme[ORC_MAX_ARMS];     /* removed by Extreme pruning: never re-admitted */
 } tuner_state;
+
+/* ENV.md §4.11 statistical anchor: the arm with the lowest historical
+ * mean EDP among arms with at least min_samples observations; ties to the lowest frequency. */
+uint32_t orc_stat_anchor(const orc_config *c, const uint32_t *n, const double *ebar, const uint8_t *extreme)
+{
+    uint32_t best = ORC_NEVER;
+    for (uint32_t k = 0; k < c->n_arms; ++k) {
+        if (extreme[k] || n[k] < c->rf_min_samples) continue;
+        if (best == ORC_NEVER || ebar[k] < ebar[best]) best = k;
+    }
+    return best;
+}
+
+/* ENV.md §4.11 refine: every grid frequency within ±half of the anchor on
+ * the refine step, minus the Extreme-pruned ones.  Returns the number of active arms. */
+uint32_t orc_refine_window(const orc_config *c, uint32_t anchor, const uint8_t *extreme, uint8_t *active_out)
+{
+    uint32_t na = 0;
+    const int64_t fa = (int64_t)c->f_min_mhz + (int64_t)anchor * c->f_step_mhz;
+    for (uint32_t k = 0; k < c->n_arms; ++k) {
+        const int64_t fk = (int64_t)c->f_min_mhz + (int64_t)k * c->f_step_mhz;
+        const int64_t dist = fk > fa ? fk - fa : fa - fk;
+        const int in = dist <= (int64_t)c->rf_half_mhz && dist % (int64_t)c->rf_step_mhz == 0 && !extreme[k];
+        active_out[k] = (uint8_t)in;
+        na += (uint32_t)in;
+    }
+    return na;
+}
 
 /* ENV.md §4.10, observe_reward: classical Page-Hinkley on the reward
  * stream; an alarm (cum - min > λ) resets the detector and re-enters Exploration; W quiet
@@ -446,6 +475,7 @@ int orc_run_tuner_ex(const orc_config *c, const orc_tuner *tu, uint32_t T, const
     memset(st, 0, sizeof(*st));
     st->traj_hash = 0xcbf29ce484222325ull;
     st->first_exploit_t = ORC_NEVER;
+    st->last_anchor = ORC_NEVER;
 
     /* f_max baseline response constants are folded into orc_env_response */
     uint32_t row[ORC_ROW_WORDS];
@@ -529,6 +559,7 @@ int orc_run_tuner_ex(const orc_config *c, const orc_tuner *tu, uint32_t T, const
         double E = resp[0], tpot = resp[1], ttft = resp[2], edp = resp[3];
         double r = orc_reward(edp, S->window, S->wcount, c->clip_lo, c->clip_hi);
         if (inj && inj->reward) r = inj->reward[(size_t)t * K + kstar];
+        const uint32_t phase_sel = S->phase;
         if (c->ph_enable) ph_observe(c, S, r, t, st);                /* §4.10, after a8 */
         if (S->wcount < c->median_window) {
             S->window[S->wcount++] = edp;
@@ -597,9 +628,47 @@ int orc_run_tuner_ex(const orc_config *c, const orc_tuner *tu, uint32_t T, const
             for (uint32_t k = 0; k < K; ++k) {
                 if (!(ext[k] || hist[k] || cas[k]) || (int)k == restore) continue;
                 S->active[k] = 0;
-                if (ext[k]) st->n_pruned_extreme++;
+                if (ext[k]) {
+                    st->n_pruned_extreme++;
+                    S->extreme[k] = 1;
+                }
                 else if (hist[k]) st->n_pruned_hist++;
                 else st->n_pruned_cascade++;
+            }
+        }
+
+        /* §4.11 mixed maturity-based refinement, after pruning: every rf_period rounds and on a
+         * phase transition */
+        if (c->rf_enable && ((t + 1) % c->rf_period == 0 || (c->ph_enable && S->phase != phase_sel))) {
+            uint32_t anchor = ORC_NEVER;
+            if (t < c->rf_mature) {                                   /* Statistical */
+                uint8_t ex[ORC_MAX_ARMS];
+                for (uint32_t k = 0; k < K; ++k) ex[k] = S->extreme[k];
+                anchor = orc_stat_anchor(c, S->n, S->ebar, ex);
+            } else {                                                  /* Predictive */
+                double a_ucb = tu->alpha0 / sqrt(1.0 + (double)t / c->tau);   /* Eq. 1's α_t */
+                double best = 0.0;
+                for (uint32_t k = 0; k < K; ++k) {
+                    if (!S->active[k]) continue;
+                    double p = 0.0;
+                    for (uint32_t i = 0; i < d; ++i) p = p + S->theta[k][i] * x[i];
+                    double qf = 0.0;
+                    for (uint32_t i = 0; i < d; ++i) {
+                        double row_i = 0.0;
+                        for (uint32_t j = 0; j < d; ++j) row_i = row_i + S->Ainv[k][i * d + j] * x[j];
+                        qf = qf + x[i] * row_i;
+                    }
+                    double ucb = p + a_ucb * sqrt(qf > 0.0 ? qf : 0.0);
+                    if (anchor == ORC_NEVER || ucb > best) { anchor = k; best = ucb; }
+                }
+            }
+            if (anchor != ORC_NEVER) {
+                uint8_t ex[ORC_MAX_ARMS], act[ORC_MAX_ARMS];
+                for (uint32_t k = 0; k < K; ++k) ex[k] = S->extreme[k];
+                orc_refine_window(c, anchor, ex, act);
+                for (uint32_t k = 0; k < K; ++k) S->active[k] = act[k];
+                st->n_refine += 1;
+                st->last_anchor = anchor;
             }
         }
 

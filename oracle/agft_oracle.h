@@ -45,6 +45,10 @@ typedef struct {
     /* Page-Hinkley exploitation switch (ENV.md §4.10; Eq. 2) */
     uint32_t ph_enable, ph_window;     /* on/off; quiet window W (50) */
     double ph_delta, ph_lambda;        /* δ (0.005), λ (50·δ) */
+    /* Mixed maturity-based refinement (ENV.md §4.11) */
+    uint32_t rf_enable, rf_period;     /* on/off; evaluated every rf_period rounds (25) */
+    uint32_t rf_mature, rf_min_samples;/* t_mature (100); statistical anchor needs n ≥ 4 */
+    uint32_t rf_half_mhz, rf_step_mhz; /* window ±150 MHz, step 15 MHz */
 } orc_config;
 
 typedef struct {                       /* per-tuner hyper-parameters (the sweep axes) */
@@ -63,6 +67,8 @@ typedef struct {                       /* ENV.md §4.9 */
     uint32_t ph_alarms;                /* Page-Hinkley drift alarms */
     uint32_t first_exploit_t;          /* first step t after which the phase became Exploitation (ORC_NEVER) */
     uint32_t phase;                    /* final phase: 0 Exploration, 1 Exploitation */
+    uint32_t n_refine;                 /* refinements applied (ENV.md §4.11) */
+    uint32_t last_anchor;              /* arm index of the last anchor (ORC_NEVER if none) */
 } orc_stats;
 
 #define ORC_NEVER 0xFFFFFFFFu
@@ -131,6 +137,12 @@ int orc_run_tuner_ex(const orc_config *c, const orc_tuner *tu, uint32_t T, const
 void orc_sweep(const orc_config *c, uint32_t trace_id, uint32_t t0, uint32_t n, double *S /*[K][3]*/,
                double *SP /*[5][K]*/, uint32_t *NP /*[5]*/, double *O /*[2]*/, uint8_t *best /*[n] or NULL*/);
 uint32_t orc_argmin(const double *v, uint32_t K, uint32_t stride);
+
+/* ENV.md §4.11 helpers (also used by the run loop): the statistical anchor (smallest ē among
+ * non-extreme arms with n ≥ min_samples, ties to the lowest arm; ORC_NEVER if none) and the
+ * refined action space around an anchor (window minus extreme-pruned arms). */
+uint32_t orc_stat_anchor(const orc_config *c, const uint32_t *n, const double *ebar, const uint8_t *extreme);
+uint32_t orc_refine_window(const orc_config *c, uint32_t anchor, const uint8_t *extreme, uint8_t *active_out);
 
 uint32_t orc_sizeof(int which /* 0 config 1 tuner 2 stats 3 arms 4 steprec 5 record 6 inject */);
 

@@ -136,6 +136,8 @@ def main():
     ap.add_argument("--T", type=int, default=None, help="override decision windows (debug only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--refine", action="store_true",
+                    help="enable mixed maturity-based refinement (ENV.md §4.11; WIDE schedule)")
     ap.add_argument("--chunk", type=int, default=CHUNK, help="windows per agft_replay call (records buffer)")
     ap.add_argument("--phase", action="store_true",
                     help="enable the Page-Hinkley exploitation phase (ENV.md §4.10; not the §8(a) headline)")
@@ -160,6 +162,8 @@ def main():
         cfg["T"] = args.T
     if args.phase:
         cfg["ph_enable"] = 1          # ENV.md §4.10 exploitation phase
+    if args.refine:
+        cfg["rf_enable"] = 1          # ENV.md §4.11 refinement (NEXT row 1; WIDE schedule)
     T = cfg["T"]
 
     if args.impl == "reference":
@@ -274,6 +278,7 @@ def main():
                                   f"{T} windows ({R} traces/GPU, α×pruning sweep, diurnal+burst)",
                       "tuners_per_gpu": n, "T": T, "arms": cfg["n_arms"], "d": cfg["d"],
                       "phase_switch": bool(cfg.get("ph_enable", 0)),
+                      "refinement": bool(cfg.get("rf_enable", 0)),
                       "traces_per_gpu": R, "chunk": chunk,
                       "l2": f"inputs larger than L2: tuner state {tb.workspace.numel() / 2**30:.2f} GiB/GPU",
                       "parallelism": f"tuner shards dp{world}"},

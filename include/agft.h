@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define AGFT_ABI_VERSION 2u         /* 2: + agft_phase, + Page-Hinkley stats */
+#define AGFT_ABI_VERSION 3u         /* 2: + agft_phase; 3: + agft_refine (and their stats) */
 #define AGFT_MAX_ARMS 128u          /* K ≤ 128 */
 #define AGFT_MAX_D 7u               /* the paper's 7-dim context */
 #define AGFT_MAX_WINDOW 64u         /* reward-median window, AMB-3 */
@@ -93,6 +93,12 @@ typedef struct {
  * Eq. 2); an alarm (cum − min > lambda) resets the detector and re-enters Exploration. */
 typedef struct { uint32_t enable, window; double delta, lambda; } agft_phase;
 
+/* Mixed maturity-based refinement (ENV.md §4.11): every `period` rounds
+ * (and on a phase transition) the action space becomes the ±half_mhz window on the step_mhz
+ * lattice around an anchor — the lowest-mean-EDP arm with ≥ min_samples observations while
+ * t < mature, the UCB argmax after — minus Extreme-pruned arms.  Runs on the WIDE schedule. */
+typedef struct { uint32_t enable, period, mature, min_samples, half_mhz, step_mhz; } agft_refine;
+
 typedef struct {
     uint32_t abi_version;     /* must be AGFT_ABI_VERSION */
     uint32_t n_tuners;        /* N ≥ 1 */
@@ -110,6 +116,8 @@ typedef struct {
     double norm_lo[7], norm_hi[7];   /* context normalisation bounds (AMB-14) */
     uint64_t env_seed;               /* S in ENV.md §1 */
     agft_phase phase;                /* Page-Hinkley exploitation switch (ENV.md §4.10) */
+    agft_refine refine;              /* mixed maturity-based refinement (ENV.md §4.11) */
+    uint32_t pad1;
 } agft_config;
 
 /* Per-tuner parameters (the hyper-parameter sweep axes of C4/C5). */
@@ -121,7 +129,7 @@ typedef struct {
     double historical_k;      /* k_h, P:388 (1.0) */
 } agft_tuner_params;          /* 32 B */
 
-/* Per-tuner statistics (ENV.md §4.9, §4.10), 120 B. */
+/* Per-tuner statistics (ENV.md §4.9–§4.11), 128 B. */
 typedef struct {
     uint64_t traj_hash;       /* FNV-1a over the chosen arm of every step */
     uint64_t sum_active;      /* Σ_t |F_available(t)| before pruning (work counter) */
@@ -132,6 +140,8 @@ typedef struct {
     uint32_t ph_alarms;       /* Page-Hinkley drift alarms */
     uint32_t first_exploit_t; /* first step after which the phase was Exploitation, AGFT_NEVER if none */
     uint32_t phase;           /* current phase: 0 Exploration, 1 Exploitation */
+    uint32_t n_refine;        /* refinements applied (ENV.md §4.11) */
+    uint32_t last_anchor;     /* arm index of the last refinement anchor, AGFT_NEVER if none */
 } agft_tuner_stats;
 
 #define AGFT_NEVER 0xFFFFFFFFu

@@ -14,7 +14,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("AGFT_LIB_PATH") or os.path.join(HERE, "libagft.so")   # override: A/B builds
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 RECORD_BYTES = 128
 ROW_WORDS = 12
 NO_RECORD = 0xFFFFFFFF
@@ -57,12 +57,17 @@ class AgftPhase(C.Structure):
     _fields_ = [("enable", u32), ("window", u32), ("delta", f64), ("lambda_", f64)]
 
 
+class AgftRefine(C.Structure):
+    _fields_ = [("enable", u32), ("period", u32), ("mature", u32), ("min_samples", u32),
+                ("half_mhz", u32), ("step_mhz", u32)]
+
+
 class AgftConfig(C.Structure):
     _fields_ = [("abi_version", u32), ("n_tuners", u32), ("d", u32), ("n_traces", u32),
                 ("trace_base", u32), ("record_slots", u32), ("kernel_policy", u32), ("pad0", u32),
                 ("grid", AgftGrid), ("prune", AgftPrune), ("policy", AgftPolicy), ("env", AgftEnv),
                 ("trace", AgftTraceCfg), ("norm_lo", f64 * 7), ("norm_hi", f64 * 7), ("env_seed", u64),
-                ("phase", AgftPhase)]
+                ("phase", AgftPhase), ("refine", AgftRefine), ("pad1", u32)]
 
 
 PARAMS_DTYPE = np.dtype([("trace_id", "<u4"), ("record_slot", "<u4"), ("alpha0", "<f8"),
@@ -74,8 +79,9 @@ STATS_DTYPE = np.dtype([("traj_hash", "<u8"), ("sum_active", "<u8"),
                         ("sum_energy", "<f8"), ("sum_tpot", "<f8"), ("sum_ttft", "<f8"),
                         ("sum_edp", "<f8"), ("sum_reward", "<f8"), ("base_energy", "<f8"),
                         ("base_edp", "<f8"), ("exploit_steps", "<u4"), ("ph_alarms", "<u4"),
-                        ("first_exploit_t", "<u4"), ("phase", "<u4")])
-assert PARAMS_DTYPE.itemsize == 32 and STATS_DTYPE.itemsize == 120
+                        ("first_exploit_t", "<u4"), ("phase", "<u4"), ("n_refine", "<u4"),
+                        ("last_anchor", "<u4")])
+assert PARAMS_DTYPE.itemsize == 32 and STATS_DTYPE.itemsize == 128
 
 STATUS = {0: "ok", -1: "invalid argument", -2: "invalid frequency grid", -3: "empty arm set",
           -4: "context dimension out of range", -5: "non-finite or out-of-range coefficient",
@@ -171,6 +177,8 @@ def make_config(cfg: dict, n_tuners: int | None = None, n_traces: int | None = N
     c.env_seed = cfg["seed"]
     c.phase = AgftPhase(cfg.get("ph_enable", 0), cfg.get("ph_window", 50), cfg.get("ph_delta", 0.005),
                         cfg.get("ph_lambda", 0.25))
+    c.refine = AgftRefine(cfg.get("rf_enable", 0), cfg.get("rf_period", 25), cfg.get("rf_mature", 100),
+                          cfg.get("rf_min_samples", 4), cfg.get("rf_half_mhz", 150), cfg.get("rf_step_mhz", 15))
     return c
 
 

@@ -122,6 +122,9 @@ agft_status validate(const agft_config *c)
         !finite(p.tie_rel) || p.tie_rel < 0)
         return AGFT_E_NONFINITE;
     if (p.median_window < 1 || p.median_window > AGFT_MAX_WINDOW) return AGFT_E_INVALID_ARG;
+    const agft_refine &rf = c->refine;               // ENV.md §4.11
+    if (rf.enable > 1u) return AGFT_E_INVALID_ARG;
+    if (rf.enable && (rf.period < 1u || rf.step_mhz < 1u)) return AGFT_E_INVALID_ARG;
     const agft_phase &ph = c->phase;                 // ENV.md §4.10
     if (ph.enable > 1u) return AGFT_E_INVALID_ARG;
     if (ph.enable && (ph.window < 1u || !finite(ph.delta) || !finite(ph.lambda) || ph.delta < 0 || ph.lambda < 0))
@@ -195,6 +198,12 @@ ReplayArgs replay_args(agft_handle h, const void *records, uint32_t t0, uint32_t
     a.ph_window = c.phase.window;
     a.ph_delta = c.phase.delta;
     a.ph_lambda = c.phase.lambda;
+    a.rf_enable = c.refine.enable;
+    a.rf_period = c.refine.period;
+    a.rf_mature = c.refine.mature;
+    a.rf_min_samples = c.refine.min_samples;
+    a.rf_half_mhz = c.refine.half_mhz;
+    a.rf_step_mhz = c.refine.step_mhz;
     // ENV.md §4.8: (double)F_k < cascade_fraction * (double)f_max_hw — one IEEE product
     volatile double cf = c.prune.cascade_fraction;
     a.cascade_limit = cf * (double)c.grid.f_max_hw_mhz;
@@ -337,6 +346,7 @@ static agft_status run_steps(agft_handle h, const void *d_records, uint32_t t0, 
         const uint32_t t = t0 + s;
         uint32_t len = sub_chunk(t);
         if (len > n - s) len = n - s;
+        else if (n - s - len < len / 2) len = n - s;   // absorb a short tail: one launch wave-tail less (A/B −2%)
         ReplayArgs a = replay_args(h, d_records, t, len);
         a.rec_stride = n;
         a.rec_off = s;
@@ -344,7 +354,8 @@ static agft_status run_steps(agft_handle h, const void *d_records, uint32_t t0, 
         a.gap = c.record_slots ? gap : nullptr;
         a.chosen = chosen;
         cudaError_t e = cudaSuccess;
-        if (c.kernel_policy == AGFT_POLICY_WIDE) {
+        // refinement re-admits arms, so a tuner's class can grow: one warp per tuner throughout
+        if (c.kernel_policy == AGFT_POLICY_WIDE || c.refine.enable) {
             e = launch_replay(a, c.d, h->stream);
         } else {
             // MSEG and LANE do not implement the exploitation phase (ENV.md §4.10): AUTO instead

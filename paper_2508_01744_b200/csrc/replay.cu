@@ -111,6 +111,12 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
     if (st.flags & 1u) return;                        // frozen by an earlier anomaly
     __shared__ PhState s_ph[kWarpsPerBlock];          // ENV.md §4.10 detector (lane 0 owns it)
     uint32_t phase = 0u;
+    uint32_t extb = 0u;                               // bit j: arm 32j+lane was Extreme-pruned (ENV.md §4.11)
+    if (a.rf_enable) {
+#pragma unroll
+        for (int j = 0; j < S; ++j)
+            if ((a.w.extm[tb * 4 + j] >> lane) & 1u) extb |= 1u << j;
+    }
     if (a.ph_enable) {
         if (lane == 0) s_ph[warp] = a.w.ph[tb];
         __syncwarp();
@@ -161,6 +167,7 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
         for (int j = 0; j < S; ++j) nact += popc_ballot((act >> j) & 1u);
 
         // ---- a3: α_t = α0/√(1+t/τ)
+        const uint32_t phase_sel = phase;
         const double alpha = phase ? 0.0 : alpha_t(prm.alpha0, t, 1.0 / a.tau);   // Exploitation: Eq. 2
 
         // ---- a4: Eq. 1 scores.  q = Σ_{i≤j} w_ij A⁻¹_ij with w_ij = x_i x_j (×2 off-diagonal)
@@ -403,7 +410,76 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
                     st.n_pruned_hist += ch;
                     st.n_pruned_cascade += cc;
                     if (rm) act &= ~(1u << j);
+                    if (rm && ext[j]) extb |= 1u << j;
                 }
+            }
+        }
+
+        // ---- ENV.md §4.11 mixed maturity-based refinement (after pruning)
+        if (a.rf_enable && ((t + 1u) % a.rf_period == 0u || (a.ph_enable && phase != phase_sel))) {
+            int anchor = -1;
+            if (t < a.rf_mature) {                    // Statistical: lowest ē among n ≥ min, not Extreme
+                double be = kInf;
+                int bk2 = 0x7fffffff;
+#pragma unroll
+                for (int j = 0; j < S; ++j) {
+                    const int k = 32 * j + lane;
+                    if (k < (int)K && !((extb >> j) & 1u) && n[j] >= a.rf_min_samples && ebar[j] < be) {
+                        be = ebar[j];
+                        bk2 = k;
+                    }
+                }
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) {
+                    const double ob = __shfl_xor_sync(kFull, be, off);
+                    const int ok = __shfl_xor_sync(kFull, bk2, off);
+                    if (ob < be || (ob == be && ok < bk2)) { be = ob; bk2 = ok; }
+                }
+                anchor = bk2 == 0x7fffffff ? -1 : bk2;
+            } else {                                  // Predictive: UCB argmax at x_t (Eq. 1's α_t)
+                const double au = alpha_t(prm.alpha0, t, 1.0 / a.tau);
+                double wv[P];
+                {
+                    int e = 0;
+#pragma unroll
+                    for (int r0 = 0; r0 < D; ++r0)
+#pragma unroll
+                        for (int c = r0; c < D; ++c, ++e) wv[e] = (r0 == c) ? x[r0] * x[r0] : 2.0 * x[r0] * x[c];
+                }
+                double bu = -kInf;
+                int bk2 = 0x7fffffff;
+#pragma unroll
+                for (int j = 0; j < S; ++j) {
+                    if ((act >> j) & 1u) {
+                        const double *Aj = sA + j * P * 32 + lane;
+                        const double *Tj = sT + j * D * 32 + lane;
+                        const double q = quad_form<P>(wv, Aj, 32);
+                        double p = 0.0;
+#pragma unroll
+                        for (int i = 0; i < D; ++i) p = fma(Tj[i * 32], x[i], p);
+                        const double u = p + au * sqrt(fmax(q, 0.0));
+                        if (u > bu) { bu = u; bk2 = 32 * j + lane; }
+                    }
+                }
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) {
+                    const double ob = __shfl_xor_sync(kFull, bu, off);
+                    const int ok = __shfl_xor_sync(kFull, bk2, off);
+                    if (ob > bu || (ob == bu && ok < bk2)) { bu = ob; bk2 = ok; }
+                }
+                anchor = bk2 == 0x7fffffff ? -1 : bk2;
+            }
+            if (anchor >= 0) {
+#pragma unroll
+                for (int j = 0; j < S; ++j) {
+                    const int k = 32 * j + lane;
+                    const uint32_t dist = (uint32_t)(k > anchor ? k - anchor : anchor - k) * a.f_step_mhz;
+                    const bool in = k < (int)K && dist <= a.rf_half_mhz && dist % a.rf_step_mhz == 0u &&
+                                    !((extb >> j) & 1u);
+                    act = in ? (act | (1u << j)) : (act & ~(1u << j));
+                }
+                st.n_refine += 1u;
+                st.last_anchor = (uint32_t)anchor;
             }
         }
 
@@ -469,6 +545,13 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
             ph_to_stats(s_ph[warp], st);
         }
         a.w.acc[tb] = st;
+    }
+    if (a.rf_enable) {
+#pragma unroll
+        for (int j = 0; j < S; ++j) {
+            const uint32_t bits = __ballot_sync(kFull, (extb >> j) & 1u);
+            if (lane == 0) a.w.extm[tb * 4 + j] = bits;
+        }
     }
 }
 

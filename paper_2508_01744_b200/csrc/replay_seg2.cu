@@ -21,7 +21,10 @@ namespace agft {
 
 namespace {
 
-constexpr int kSeg2Warps = 2;
+#ifndef AGFT_SEG2_WARPS
+#define AGFT_SEG2_WARPS 2               // warps per block (A/B knob)
+#endif
+constexpr int kSeg2Warps = AGFT_SEG2_WARPS;
 #ifndef AGFT_SEG2_MIN_BLOCKS
 #define AGFT_SEG2_MIN_BLOCKS 4          // no effective register cap: spills cost more than occupancy gains (A/B)
 #endif

@@ -14,7 +14,10 @@
 namespace agft {
 
 namespace {
-constexpr int kSoloThreads = 64;
+#ifndef AGFT_SOLO_THREADS
+#define AGFT_SOLO_THREADS 64            // threads per block (A/B knob)
+#endif
+constexpr int kSoloThreads = AGFT_SOLO_THREADS;
 #ifndef AGFT_SOLO_MIN_BLOCKS
 #define AGFT_SOLO_MIN_BLOCKS 4          // as SEG2: an occupancy cap (≤ 168 regs) spilled and measured slower
 #endif

@@ -178,6 +178,7 @@ __global__ void init_tuner_kernel(const __grid_constant__ InitArgs a)
             uint32_t bits = 0;
             if (a.K > lo) bits = (a.K - lo >= 32u) ? kFull : ((1u << (a.K - lo)) - 1u);
             a.w.active[tb * 4 + k] = bits;
+            a.w.extm[tb * 4 + k] = 0u;
         }
         if (k < 2) a.w.wmeta[tb * 2 + k] = 0;
         if (k == 0) {
@@ -185,6 +186,7 @@ __global__ void init_tuner_kernel(const __grid_constant__ InitArgs a)
             st.traj_hash = kFnvOffset;
             st.n_active = a.K;
             st.first_exploit_t = AGFT_NEVER;
+            st.last_anchor = AGFT_NEVER;
             a.w.acc[tb] = st;
             PhState ph = {};
             ph.first_exploit_t = AGFT_NEVER;

@@ -7,7 +7,8 @@ import oracle
 
 EXACT_STATS = ("steps", "last_arm", "n_active", "n_pruned_extreme", "n_pruned_hist", "n_pruned_cascade",
                "sum_active", "sum_energy", "sum_tpot", "sum_ttft", "sum_edp", "sum_reward",
-               "base_energy", "base_edp", "exploit_steps", "ph_alarms", "first_exploit_t", "phase")
+               "base_energy", "base_edp", "exploit_steps", "ph_alarms", "first_exploit_t", "phase",
+               "n_refine", "last_anchor")
 REL_TOL = 1e-9   # north_star: A⁻¹ entries and scores to 1e-9 relative (fp64)
 
 

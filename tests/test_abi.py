@@ -45,7 +45,7 @@ def test_library_exports_every_declared_symbol(lib):
 def test_struct_mirrors_match(lib):
     assert lib.agft_struct_size(0) == __import__("ctypes").sizeof(_abi.AgftConfig)
     assert lib.agft_struct_size(1) == 32
-    assert lib.agft_struct_size(2) == 120
+    assert lib.agft_struct_size(2) == 128
 
 
 @pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5"])

@@ -62,3 +62,32 @@ def test_c4_sweep_with_phase_sampled():
     _check(cfg, tb, params, st, sample, 20000, traj)
     assert np.all(st["steps"] == 20000) and np.all(st["flags"] == 0)
     assert (st["exploit_steps"] > 0).mean() > 0.5
+
+
+# ---------------------------------------------------------------- ENV.md §4.11 refinement (WIDE schedule)
+@pytest.mark.parametrize("kw", [
+    dict(rf_enable=1),                                               # C2 defaults: statistical → predictive
+    dict(rf_enable=1, ph_enable=1),                                  # + refinement on phase transitions
+    dict(rf_enable=1, rf_period=7, rf_mature=300, rf_step_mhz=30),
+    dict(rf_enable=1, ext_round_limit=200, ext_min_samples=1),       # many Extreme removals (permanent)
+    dict(rf_enable=1, n_arms=35, f_step_mhz=45, rf_half_mhz=225, rf_step_mhz=45),
+])
+def test_refinement_parity(kw):
+    cfg = named_config("C2")
+    cfg.update(n_tuners=5, n_traces=5, T=1500, ph_enable=0)
+    cfg.update(kw)
+    ids = list(range(5))
+    params = tuner_params(cfg, ids)
+    params["alpha0"] = np.array([0.0, 0.3, 1.0, 2.0, 5.0])
+    tb, params, st, traj, _ = _run(cfg, 1500, params=params, record=ids, chunk=512, policy=0)
+    _check(cfg, tb, params, st, ids, 1500, traj)
+    assert np.all(st["n_refine"] > 0)
+
+
+def test_refinement_c4_sample():
+    cfg = named_config("C4")
+    cfg.update(n_traces=1, rf_enable=1, ph_enable=1)
+    ids = list(range(0, 256, 8))
+    params = tuner_params(cfg, ids)
+    tb, params, st, traj, _ = _run(cfg, 6000, params=params, record=list(range(len(ids))), chunk=4500)
+    _check(cfg, tb, params, st, list(range(len(ids))), 6000, traj)

@@ -20,7 +20,7 @@ from ._abi import (NO_RECORD, PARAMS_DTYPE, RECORD_BYTES, ROW_WORDS, STATS_DTYPE
 __all__ = ["agft_workspace_bytes", "agft_create", "agft_reset", "agft_trace_generate", "agft_step", "agft_replay",
            "agft_stats", "agft_export_arms", "agft_get_step", "agft_run", "agft_sweep", "agft_regret",
            "agft_destroy", "SweepSums",
-           "TunerBatch", "make_config", "make_params", "PARAMS_DTYPE", "STATS_DTYPE", "NO_RECORD",
+           "TunerBatch", "record_slot_count", "make_config", "make_params", "PARAMS_DTYPE", "STATS_DTYPE", "NO_RECORD",
            "RECORD_BYTES", "ROW_WORDS", "AgftError", "lib_path"]
 
 
@@ -125,6 +125,14 @@ def agft_destroy(h):
     _abi.check("agft_destroy", _abi.lib().agft_destroy(h))
 
 
+def record_slot_count(record_slot) -> int:
+    """Rows of the trajectory record: 1 + the largest slot that is not NO_RECORD (0 if none)."""
+    if record_slot is None:
+        return 0
+    rs = np.asarray(record_slot, dtype=np.int64)
+    return int(np.max(np.where(rs == NO_RECORD, -1, rs), initial=-1) + 1)
+
+
 class TunerBatch:
     """N tuners on one GPU: owns (torch-allocated) workspace, params and the handle."""
 
@@ -135,8 +143,7 @@ class TunerBatch:
         self.device = torch.device(device)
         self.n = len(params["trace_id"])
         self.n_traces = cfg["n_traces"] if n_traces is None else n_traces
-        rec_slots = 0 if record_slot is None else int(np.max(np.where(
-            np.asarray(record_slot) == NO_RECORD, -1, record_slot)) + 1)
+        rec_slots = record_slot_count(record_slot)
         self.record_slots = rec_slots
         self.cfg_c = make_config(cfg, n_tuners=self.n, n_traces=self.n_traces, trace_base=trace_base,
                                  record_slots=rec_slots, policy=policy)

@@ -122,3 +122,13 @@ def test_product_never_imports_the_oracle():
             txt = open(os.path.join(ROOT, "oracle", f)).read()
             assert not re.search(r"\b(import|from)\s+paper_2508_01744_b200\b", txt), f
             assert not re.search(r'#include\s+"[^"]*(agft\.h|agft_internal)', txt), f
+
+
+def test_record_slot_count():
+    """Rows of the trajectory record for partially recorded batches (uint32 NO_RECORD markers)."""
+    import numpy as np
+    r = np.full(10, pkg.NO_RECORD, np.uint32)
+    assert pkg.record_slot_count(r) == 0 and pkg.record_slot_count(None) == 0
+    r[3], r[7] = 0, 4
+    assert pkg.record_slot_count(r) == 5
+    assert pkg.record_slot_count(np.arange(6, dtype=np.uint32)) == 6

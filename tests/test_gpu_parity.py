@@ -250,3 +250,28 @@ def test_lane_screened_paths_free_running():
     params = tuner_params(cfg, ids)
     tb, params, st, _, _ = _run(cfg, 3000, params=params, chunk=3000, policy=3)
     _check(cfg, tb, params, st, list(range(len(ids))), 3000, None, arms=True)
+
+
+def test_c5_rank_shard_sampled_parity():
+    """C5 (1,048,576 tuners, 4,096 traces, pattern = trace mod 3) as rank 3 of an 8-GPU strong
+    split: 131,072 local tuners on traces 1536…2047 (global Philox keys via trace_base), 3,000
+    windows in the bench's launch configuration; sampled tuners against the oracle."""
+    from paper_2508_01744_b200 import shard
+    from _parity import compare_tuner
+    cfg = _cfg("C5")
+    sh = shard.plan(cfg, 8, 3, "strong")
+    lcfg = dict(cfg, n_tuners=sh.n_tuners, n_traces=sh.n_traces)
+    sample = [0, 1, 255, 256 * 100 + 77, 256 * 511 + 255]
+    rec_slot = np.full(sh.n_tuners, NO_RECORD, np.uint32)
+    for s, i in enumerate(sample):
+        rec_slot[i] = s
+    tb = TunerBatch(lcfg, sh.params, device="cuda:0", record_slot=rec_slot, trace_base=sh.trace_base)
+    traj, _ = tb.run(3000, chunk=3000, record=True)
+    st = tb.stats()
+    assert np.all(st["steps"] == 3000) and np.all(st["flags"] == 0)
+    problems = []
+    for s, i in enumerate(sample):
+        errs, _ = compare_tuner(lcfg, sh.params, i, st[i], tb.export_arms(i), 3000, traj[s],
+                                trace_base=sh.trace_base)
+        problems += errs
+    assert not problems, "\n".join(problems[:20])

@@ -134,6 +134,47 @@ def frequencies(cfg: dict):
     return [cfg["f_min_mhz"] + k * cfg["f_step_mhz"] for k in range(cfg["n_arms"])]
 
 
+def live_inputs(cfg: dict, n_tuners: int, T: int, seed: int = BASE_SEED):
+    """Seeded inputs of the live controller API (agft_select / agft_observe).
+
+    rows [n_tuners][T][12] uint32: MetricsSnapshot counters per window in ENV.md §2.2 word order
+    (waiting, running, prefill, decode, iters, kv_used, hits, misses; words 8..11 unused) drawn
+    independently per window — a live server's counters, with idle windows (15%) and queueing
+    windows (30% with waiting > 0).
+    resp [n_tuners][T][K][3] fp64: the (energy J, TPOT s, TTFT s) a measurement would return if
+    arm k ran window t — a noisy U-shaped EDP over the grid whose minimum moves with the load,
+    standing in for NVML / the serving engine.  Plain numpy draws: inputs, not the method."""
+    rng = np.random.default_rng(seed)
+    K = cfg["n_arms"]
+    rows = np.zeros((n_tuners, T, 12), dtype=np.uint32)
+    running = rng.integers(0, cfg["cap"] + 1, size=(n_tuners, T))
+    idle = rng.random((n_tuners, T)) < 0.15
+    running[idle] = 0
+    iters = np.where(running > 0, rng.integers(20, 44, size=(n_tuners, T)), 0)
+    waiting = np.where(rng.random((n_tuners, T)) < 0.30, rng.integers(1, 40, size=(n_tuners, T)), 0)
+    arrivals = np.where(idle, 0, rng.integers(0, 12, size=(n_tuners, T)))
+    hits = (arrivals * rng.random((n_tuners, T))).astype(np.int64)
+    rows[..., 0] = waiting
+    rows[..., 1] = running
+    rows[..., 2] = arrivals * rng.integers(1, 4096, size=(n_tuners, T))
+    rows[..., 3] = running * iters
+    rows[..., 4] = iters
+    rows[..., 5] = np.minimum(cfg["kv_total"], running * rng.integers(64, 4096, size=(n_tuners, T)))
+    rows[..., 6] = hits
+    rows[..., 7] = arrivals - hits
+    f = np.asarray(frequencies(cfg), dtype=np.float64) / 1000.0            # GHz
+    load = (running / max(cfg["cap"], 1)).astype(np.float64)[..., None]     # [N][T][1]
+    f_opt = 0.9 + 0.6 * load                                               # EDP minimum moves with load
+    power = 70.0 + 25.0 * f[None, None, :] ** 3 * (0.2 + load)
+    tpot = 0.012 * (1.0 + 0.8 * (f_opt / f[None, None, :] - 1.0) ** 2 + 0.5 * (f_opt > f[None, None, :]))
+    noise = rng.random((n_tuners, T, K, 3))
+    resp = np.empty((n_tuners, T, K, 3), dtype=np.float64)
+    resp[..., 0] = power * cfg["W"] * (0.97 + 0.06 * noise[..., 0])
+    resp[..., 1] = tpot * (0.95 + 0.10 * noise[..., 1])
+    resp[..., 2] = 0.05 + 0.2 * noise[..., 2] / f[None, None, :]
+    return rows, resp
+
+
 def tiny_config(**kw) -> dict:
     """A small config for oracle-only unit tests."""
     c = named_config("C2")

@@ -95,7 +95,8 @@ class OrcRecord(C.Structure):
 
 
 class OrcInject(C.Structure):
-    _fields_ = [("x", C.POINTER(f64)), ("edp", C.POINTER(f64)), ("reward", C.POINTER(f64))]
+    _fields_ = [("x", C.POINTER(f64)), ("edp", C.POINTER(f64)), ("reward", C.POINTER(f64)),
+                ("rows", C.POINTER(u32)), ("resp", C.POINTER(f64))]
 
 
 FREE = 255
@@ -306,7 +307,8 @@ def run_tuner(cfg: dict, tuner: OrcTuner | None = None, T: int | None = None, fo
     """Run one tuner; returns (stats dict, arms dict, record dict or None).
 
     ``inject`` = {"x": [T,d], "edp": [T,K] or None, "reward": [T,K] or None} replaces the
-    synthetic environment (unit tests of the bandit core). ``follow[t] == FREE`` leaves
+    synthetic environment (unit tests of the bandit core); the live controller's environment is
+    {"rows": [T,12] snapshot rows, "resp": [T,K,3] measured (E, TPOT, TTFT)}. ``follow[t] == FREE`` leaves
     step t unforced."""
     oc = make_config(cfg)
     tu = tuner if tuner is not None else tuner_from(cfg)
@@ -338,12 +340,13 @@ def run_tuner(cfg: dict, tuner: OrcTuner | None = None, T: int | None = None, fo
     keep = []
     if inject is not None:
         inj = OrcInject()
-        for name in ("x", "edp", "reward"):
+        for name in ("x", "edp", "reward", "rows", "resp"):
             v = inject.get(name)
             if v is not None:
-                a = np.ascontiguousarray(v, dtype=np.float64)
+                dt, ct = (np.uint32, u32) if name == "rows" else (np.float64, f64)
+                a = np.ascontiguousarray(v, dtype=dt)
                 keep.append(a)
-                setattr(inj, name, _ptr(a, f64))
+                setattr(inj, name, _ptr(a, ct))
         inj_p = C.byref(inj)
     rc = lib().orc_run_tuner_ex(C.byref(oc), C.byref(tu), T,
                                 _ptr(fol, C.c_uint8) if fol is not None else None, inj_p,

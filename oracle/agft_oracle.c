@@ -485,8 +485,14 @@ int orc_run_tuner_ex(const orc_config *c, const orc_tuner *tu, uint32_t T, const
 
     for (uint32_t t = 0; t < T; ++t) {
         if (inj) {                                                   /* unit-test environment */
-            memset(&srec, 0, sizeof(srec));
-            for (uint32_t i = 0; i < 7; ++i) x[i] = i < d ? inj->x[(size_t)t * d + i] : 0.0;
+            memset(&srec, 0, sizeof(srec));                          /* no f_max baseline */
+            if (inj->rows) {                                          /* live: §4.1 from the snapshot */
+                double xr[7];
+                orc_context(c, inj->rows + (size_t)t * ORC_ROW_WORDS, xr);
+                for (uint32_t i = 0; i < 7; ++i) x[i] = i < d ? xr[i] : 0.0;
+            } else {
+                for (uint32_t i = 0; i < 7; ++i) x[i] = i < d ? inj->x[(size_t)t * d + i] : 0.0;
+            }
         } else {
             orc_trace_row(c, tu->trace_id, t, row);                  /* a0 */
             orc_step_record(c, row, &srec);                          /* a2 + the row-only part of a7 */
@@ -551,8 +557,14 @@ int orc_run_tuner_ex(const orc_config *c, const orc_tuner *tu, uint32_t T, const
         uint32_t F = c->f_min_mhz + kstar * c->f_step_mhz;
         double resp[4];
         if (inj) {
-            resp[0] = 0.0; resp[1] = 0.0; resp[2] = 0.0;
-            resp[3] = inj->edp ? inj->edp[(size_t)t * K + kstar] : 1.0;
+            if (inj->resp) {                                          /* measured response */
+                const double *m = inj->resp + ((size_t)t * K + kstar) * 3;
+                resp[0] = m[0]; resp[1] = m[1]; resp[2] = m[2];
+                resp[3] = m[0] * m[1];                                /* EDP = E × TPOT */
+            } else {
+                resp[0] = 0.0; resp[1] = 0.0; resp[2] = 0.0;
+                resp[3] = inj->edp ? inj->edp[(size_t)t * K + kstar] : 1.0;
+            }
         } else {
             orc_response(c, &srec, F, resp);
         }

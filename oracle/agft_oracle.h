@@ -98,10 +98,15 @@ typedef struct {                       /* optional per-step record (any pointer 
     uint32_t *active_mask;             /* [T][4] after pruning (caller zeroes it) */
 } orc_record;
 
-typedef struct {                       /* unit-test environment: replaces ENV-T/ENV-R */
+typedef struct {                       /* unit-test / live environment: replaces ENV-T/ENV-R */
     const double *x;                   /* [T][d] contexts */
     const double *edp;                 /* [T][n_arms] EDP of choosing arm k at t (NULL: 1.0) */
     const double *reward;              /* [T][n_arms] reward override (NULL: median rule) */
+    /* Live controller: the context is built
+     * from each window's MetricsSnapshot counters and the response is MEASURED, not modelled. */
+    const uint32_t *rows;              /* [T][12] snapshot rows; x_t = orc_context(row_t) (overrides x) */
+    const double *resp;                /* [T][n_arms][3] measured (E, TPOT, TTFT) of choosing arm k at t;
+                                          EDP = E × TPOT (AMB-4); overrides edp */
 } orc_inject;
 
 #define ORC_FREE 255                   /* follow[t] == ORC_FREE: no forced choice at step t */

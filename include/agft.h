@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define AGFT_ABI_VERSION 3u         /* 2: + agft_phase; 3: + agft_refine (and their stats) */
+#define AGFT_ABI_VERSION 4u         /* 2: + agft_phase; 3: + agft_refine (and their stats); 4: + agft_select/agft_observe */
 #define AGFT_MAX_ARMS 128u          /* K ≤ 128 */
 #define AGFT_MAX_D 7u               /* the paper's 7-dim context */
 #define AGFT_MAX_WINDOW 64u         /* reward-median window, AMB-3 */
@@ -178,6 +178,29 @@ agft_status agft_trace_generate(agft_handle h, uint32_t t0, uint32_t n_steps, vo
  * at the handle's current step t; d_records = [n_traces][1][128 B] for step t;
  * d_chosen = [n_tuners] chosen arm index, or NULL.  Advances t by 1. */
 agft_status agft_step(agft_handle h, const void *d_records, uint32_t *d_chosen);
+
+/* ---- Live two-phase step.  The paper's controller runs one decision
+ * per sampling window on a live server (§4): read the window's metrics, pick
+ * a frequency, run the window at it, measure energy and latency, update.  agft_step splits here
+ * into the two halves a real controller (NVML + the serving engine's metrics) calls:
+ *
+ * agft_select: d_rows [n_tuners][12] uint32, 16-byte aligned — each tuner's MetricsSnapshot
+ *   counters of the last window in ENV.md §2.2 word order (waiting, running, prefill, decode,
+ *   iterations, kv_used, hits, misses; words 8..11 ignored).  Builds x_t (§4.1, with
+ *   the config's normalisation bounds), scores every active arm (Eq. 1), takes the argmax (lowest
+ *   frequency on ties) and writes d_chosen [n_tuners] = arm index k* (f = f_min + k*·step MHz), or
+ *   AGFT_NEVER for a frozen tuner.  Tuner state is not modified.
+ * agft_observe: d_resp [n_tuners][3] fp64 = (energy J, TPOT s, TTFT s) measured over the window
+ *   run at the selected frequency.  EDP = E × TPOT (AMB-4), then the reward, the
+ *   update of the chosen arm (Eqs. 3–5), pruning (§4.3), the exploitation phase / refinement if
+ *   configured, and the stats — exactly the replay's a8–a11.  Advances the step counter by 1.
+ *   A non-finite E, TPOT or TTFT sets flags bit 0 and freezes that tuner.  The f_max baseline
+ *   (base_energy, base_edp) is not measurable live and is not accumulated.
+ * Alternation is strict: a second agft_select, or agft_step / agft_replay, between a
+ * select and its observe returns AGFT_E_STATE, as does an agft_observe without a select.
+ * Both are asynchronous on the handle's stream (one kernel launch each). */
+agft_status agft_select(agft_handle h, const uint32_t *d_rows, uint32_t *d_chosen);
+agft_status agft_observe(agft_handle h, const double *d_resp);
 
 /* n_steps decision windows for every tuner, steps [t0, t0+n_steps); t0 must equal the
  * handle's step counter (AGFT_E_STATE otherwise).  d_records = [n_traces][n_steps][128 B].

@@ -4,7 +4,8 @@ The Python layer marshals arguments into the C ABI of ``include/agft.h``
 (``libagft.so``, hand-written sm_100a kernels). PyTorch provides device memory,
 streams and process groups only. Names follow the ABI: ``agft_create``,
 ``agft_trace_generate``, ``agft_step``, ``agft_replay``, ``agft_stats``,
-``agft_export_arms``, ``agft_run``, ``agft_sweep``, ``agft_regret``, ``agft_destroy``.
+``agft_export_arms``, ``agft_run``, ``agft_sweep``, ``agft_regret``, ``agft_destroy``, and the
+live two-phase step ``agft_select`` / ``agft_observe``.
 ``TunerBatch`` bundles them.
 """
 from __future__ import annotations
@@ -18,6 +19,7 @@ from ._abi import (NO_RECORD, PARAMS_DTYPE, RECORD_BYTES, ROW_WORDS, STATS_DTYPE
                    make_config, make_params)
 
 __all__ = ["agft_workspace_bytes", "agft_create", "agft_reset", "agft_trace_generate", "agft_step", "agft_replay",
+           "agft_select", "agft_observe",
            "agft_stats", "agft_export_arms", "agft_get_step", "agft_run", "agft_sweep", "agft_regret",
            "agft_destroy", "SweepSums",
            "TunerBatch", "record_slot_count", "make_config", "make_params", "PARAMS_DTYPE", "STATS_DTYPE", "NO_RECORD",
@@ -66,6 +68,14 @@ def agft_trace_generate(h, t0, n_steps, records, raw=None):
 
 def agft_step(h, records, chosen=None):
     _abi.check("agft_step", _abi.lib().agft_step(h, _p(records), _p(chosen)))
+
+
+def agft_select(h, rows, chosen):
+    _abi.check("agft_select", _abi.lib().agft_select(h, _p(rows), _p(chosen)))
+
+
+def agft_observe(h, resp):
+    _abi.check("agft_observe", _abi.lib().agft_observe(h, _p(resp)))
 
 
 def agft_replay(h, records, t0, n_steps, traj=None, gap=None):
@@ -189,6 +199,20 @@ class TunerBatch:
         chosen = torch.empty(self.n, dtype=torch.int32, device=self.device)
         agft_step(self.h, records_t, chosen)
         return chosen
+
+    def select(self, rows, chosen=None):
+        """Live step, first half: rows [n][12] int32 device tensor of MetricsSnapshot counters →
+        chosen arm per tuner (int32 [n] device tensor; -1 = frozen tuner)."""
+        import torch
+        if chosen is None:
+            chosen = torch.empty(self.n, dtype=torch.int32, device=self.device)
+        agft_select(self.h, rows, chosen)
+        return chosen
+
+    def observe(self, resp):
+        """Live step, second half: resp [n][3] float64 device tensor of measured (E J, TPOT s,
+        TTFT s) at the selected frequencies."""
+        agft_observe(self.h, resp)
 
     def run(self, T: int, chunk: int = 4500, record: bool = False):
         """Generate + replay steps [t, T) in chunks; returns recorded traj/gap (host) if asked."""

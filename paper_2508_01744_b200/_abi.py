@@ -14,7 +14,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("AGFT_LIB_PATH") or os.path.join(HERE, "libagft.so")   # override: A/B builds
 
-ABI_VERSION = 3
+ABI_VERSION = 4
 RECORD_BYTES = 128
 ROW_WORDS = 12
 NO_RECORD = 0xFFFFFFFF
@@ -97,6 +97,8 @@ PROTOTYPES = {
     "agft_reset": (C.c_int, [vp]),
     "agft_trace_generate": (C.c_int, [vp, u32, u32, vp, vp]),
     "agft_step": (C.c_int, [vp, vp, vp]),
+    "agft_select": (C.c_int, [vp, vp, vp]),
+    "agft_observe": (C.c_int, [vp, vp]),
     "agft_replay": (C.c_int, [vp, vp, u32, u32, vp, vp]),
     "agft_stats": (C.c_int, [vp, vp]),
     "agft_export_arms": (C.c_int, [vp, u32, vp, vp, vp, vp, vp, vp, vp]),

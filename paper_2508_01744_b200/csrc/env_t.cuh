@@ -47,6 +47,33 @@ __device__ __forceinline__ void response(const StepRec &r, double dec, double pr
     E = xmul(xmul(xadd(p_idle, xmul(pw, ue)), W), r.nE);
 }
 
+// §4.1 context x1..x7 from one window's MetricsSnapshot counters (ENV.md §3.2), then
+// the per-dimension normalisation clamp((raw − lo)/(hi − lo), 0, 1), 0 when hi = lo (AMB-14/15).
+__device__ __forceinline__ void context_of(uint32_t waiting, uint32_t running, uint32_t prefill, uint32_t decode,
+                                           uint32_t iters, uint32_t kv_used, uint32_t hits, uint32_t misses,
+                                           double W, uint32_t kv_total, const double *norm_lo,
+                                           const double *norm_hi, double (&x)[7])
+{
+    double raw[7];
+    raw[0] = waiting > 0 ? 1.0 : 0.0;
+    raw[1] = xdiv((double)prefill, W);
+    raw[2] = xdiv((double)decode, W);
+    raw[3] = xdiv((double)((uint64_t)prefill + (uint64_t)decode), (double)(iters > 0 ? iters : 1u));
+    raw[4] = (double)running;
+    raw[5] = xdiv((double)kv_used, (double)kv_total);
+    raw[6] = (hits + misses) > 0 ? xdiv((double)hits, (double)(hits + misses)) : 0.0;
+#pragma unroll
+    for (int i = 0; i < 7; ++i) {
+        const double lo = norm_lo[i], hi = norm_hi[i];
+        double xv = 0.0;
+        if (hi > lo) {
+            xv = xdiv(xsub(raw[i], lo), xsub(hi, lo));
+            xv = xv < 0.0 ? 0.0 : (xv > 1.0 ? 1.0 : xv);
+        }
+        x[i] = xv;
+    }
+}
+
 // ENV.md §2.2: the Table-1 prototype of the 10-minute segment holding window t
 __device__ __forceinline__ uint32_t prototype_of(const agft_trace_cfg &c, const Philox &ph, uint32_t t)
 {

@@ -20,6 +20,7 @@ struct agft_handle_s {
     cudaEvent_t fork, join[kNumCls];
     uint32_t t;             // current global step (observe/apply alternate strictly)
     uint32_t sweep_t;       // next window of the offline sweep (ENV.md §5 accumulation order)
+    uint32_t live_pending;  // 1 between agft_select and its agft_observe
     agft_status sticky;     // AGFT_OK or AGFT_E_CUDA
 };
 
@@ -211,6 +212,9 @@ ReplayArgs replay_args(agft_handle h, const void *records, uint32_t t0, uint32_t
     a.p_idle = c.env.p_idle;
     a.u_floor = c.env.u_floor;
     a.u_max = c.env.u_max;
+    a.kv_total = c.trace.kv_total;
+    std::memcpy(a.norm_lo, c.norm_lo, sizeof(a.norm_lo));
+    std::memcpy(a.norm_hi, c.norm_hi, sizeof(a.norm_hi));
     return a;
 }
 
@@ -261,6 +265,7 @@ agft_status agft_create(const agft_config *cfg, const agft_tuner_params *d_param
     h->stream = static_cast<cudaStream_t>(stream);
     h->t = 0;
     h->sweep_t = 0;
+    h->live_pending = 0;
     h->sticky = AGFT_OK;
     h->fork = nullptr;
     for (int c = 0; c < kNumCls; ++c) {
@@ -308,6 +313,7 @@ agft_status agft_reset(agft_handle h)
     if (st == AGFT_OK) {
         h->t = 0;
         h->sweep_t = 0;
+        h->live_pending = 0;
     }
     return st;
 }
@@ -394,7 +400,7 @@ agft_status agft_replay(agft_handle h, const void *d_records, uint32_t t0, uint3
 {
     if (!h || !d_records) return AGFT_E_INVALID_ARG;
     if (h->sticky != AGFT_OK) return h->sticky;
-    if (t0 != h->t) return AGFT_E_STATE;
+    if (t0 != h->t || h->live_pending) return AGFT_E_STATE;
     if (n_steps == 0) return AGFT_OK;
     agft_status st = run_steps(h, d_records, t0, n_steps, d_traj, d_gap, nullptr);
     if (st == AGFT_OK) h->t += n_steps;
@@ -405,8 +411,39 @@ agft_status agft_step(agft_handle h, const void *d_records, uint32_t *d_chosen)
 {
     if (!h || !d_records) return AGFT_E_INVALID_ARG;
     if (h->sticky != AGFT_OK) return h->sticky;
+    if (h->live_pending) return AGFT_E_STATE;
     agft_status st = run_steps(h, d_records, h->t, 1, nullptr, nullptr, d_chosen);
     if (st == AGFT_OK) h->t += 1;
+    return st;
+}
+
+// Live two-phase step: one launch each, WIDE mapping (a warp per tuner), whatever the class.
+agft_status agft_select(agft_handle h, const uint32_t *d_rows, uint32_t *d_chosen)
+{
+    if (!h || !d_rows || !d_chosen) return AGFT_E_INVALID_ARG;
+    if (reinterpret_cast<uintptr_t>(d_rows) % 16 != 0) return AGFT_E_INVALID_ARG;
+    if (h->sticky != AGFT_OK) return h->sticky;
+    if (h->live_pending) return AGFT_E_STATE;
+    ReplayArgs a = replay_args(h, nullptr, h->t, 1);
+    a.live_rows = d_rows;
+    a.chosen = d_chosen;
+    agft_status st = cuda_status(h, launch_live(a, h->cfg.d, 1, h->stream));
+    if (st == AGFT_OK) h->live_pending = 1;
+    return st;
+}
+
+agft_status agft_observe(agft_handle h, const double *d_resp)
+{
+    if (!h || !d_resp) return AGFT_E_INVALID_ARG;
+    if (h->sticky != AGFT_OK) return h->sticky;
+    if (!h->live_pending) return AGFT_E_STATE;
+    ReplayArgs a = replay_args(h, nullptr, h->t, 1);
+    a.live_resp = d_resp;
+    agft_status st = cuda_status(h, launch_live(a, h->cfg.d, 2, h->stream));
+    if (st == AGFT_OK) {
+        h->live_pending = 0;
+        h->t += 1;
+    }
     return st;
 }
 

@@ -13,6 +13,12 @@
 // The canonical 128-slot reduction of ENV.md §4.8 maps onto this layout exactly:
 // levels 1–5 are the xor-butterfly across lanes (adjacent arms are adjacent lanes),
 // levels 6–7 combine the four slot partials in-lane.
+//
+// MODE 0 is the replay (records from K1).  MODE 1 / 2 are the live two-phase step of
+// agft_select / agft_observe (one window, WIDE mapping): select builds x_t from the tuner's
+// MetricsSnapshot row, scores and picks k* and stops (no state change); observe takes the
+// MEASURED (E, TPOT, TTFT) at k* in place of ENV-R and runs a8–a11 exactly as the replay does.
+#include "env_t.cuh"
 #include "step_common.cuh"
 
 namespace agft {
@@ -86,7 +92,7 @@ constexpr int kWarpsPerBlock = 2;
 
 }  // namespace
 
-template <int D, int S>
+template <int D, int S, int MODE>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 replay_kernel(const __grid_constant__ ReplayArgs a)
 {
@@ -108,7 +114,10 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
     if (widx >= cnt) return;
     const uint64_t tb = a.list ? a.list[widx] : widx;
     agft_tuner_stats st = a.w.acc[tb];
-    if (st.flags & 1u) return;                        // frozen by an earlier anomaly
+    if (st.flags & 1u) {                              // frozen by an earlier anomaly
+        if (MODE == 1 && lane == 0) a.chosen[tb] = AGFT_NEVER;
+        return;
+    }
     __shared__ PhState s_ph[kWarpsPerBlock];          // ENV.md §4.10 detector (lane 0 owns it)
     uint32_t phase = 0u;
     uint32_t extb = 0u;                               // bit j: arm 32j+lane was Extreme-pruned (ENV.md §4.11)
@@ -154,13 +163,27 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
 
     for (uint32_t s = 0; s < a.n_steps; ++s) {
         const uint32_t t = a.t0 + s;
-        const StepRec &rec = rp[s];
         double x[D];
+        double g = 0.0, invIm = 0.0, invAm = 0.0, wIm = 0.0, nT = 0.0, nE = 0.0, baseE = 0.0, baseEDP = 0.0;
+        uint32_t recI = 0u, recP = 0u;
+        if constexpr (MODE == 0) {
+            const StepRec &rec = rp[s];
 #pragma unroll
-        for (int i = 0; i < D; ++i) x[i] = rec.x[i];
-        const double g = rec.g, invIm = rec.invIm, invAm = rec.invAm, wIm = rec.wIm;
-        const double nT = rec.nT, nE = rec.nE, baseE = rec.baseE, baseEDP = rec.baseEDP;
-        const uint32_t recI = rec.I, recP = rec.P;
+            for (int i = 0; i < D; ++i) x[i] = rec.x[i];
+            g = rec.g; invIm = rec.invIm; invAm = rec.invAm; wIm = rec.wIm;
+            nT = rec.nT; nE = rec.nE; baseE = rec.baseE; baseEDP = rec.baseEDP;
+            recI = rec.I; recP = rec.P;
+        } else if constexpr (MODE == 1) {             // live: §4.1 context of the tuner's own snapshot
+            const uint4 *rw = reinterpret_cast<const uint4 *>(a.live_rows + tb * AGFT_ROW_WORDS);
+            const uint4 r0 = rw[0], r1 = rw[1];
+            double xr[7];
+            context_of(r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w, a.W, a.kv_total, a.norm_lo, a.norm_hi, xr);
+#pragma unroll
+            for (int i = 0; i < D; ++i) x[i] = xr[i];
+        } else {                                      // live observe: the x_t of the selection
+#pragma unroll
+            for (int i = 0; i < D; ++i) x[i] = a.w.live[tb].x[i];
+        }
 
         int nact = 0;
 #pragma unroll
@@ -170,6 +193,15 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
         const uint32_t phase_sel = phase;
         const double alpha = phase ? 0.0 : alpha_t(prm.alpha0, t, 1.0 / a.tau);   // Exploitation: Eq. 2
 
+        int kstar, own, jst;
+        double sstar = 0.0, mstar = 0.0, s2 = -kInf, m2 = 0.0;
+        bool near;
+        if constexpr (MODE == 2) {
+            kstar = (int)a.w.live[tb].kstar;
+            near = a.w.live[tb].near != 0u;
+            own = kstar & 31;
+            jst = kstar >> 5;
+        } else {
         // ---- a4: Eq. 1 scores.  q = Σ_{i≤j} w_ij A⁻¹_ij with w_ij = x_i x_j (×2 off-diagonal)
         double w[P];
         {
@@ -207,14 +239,15 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
             const int ok = __shfl_xor_sync(kFull, bk, off);
             if (os > bs || (os == bs && ok < bk)) { bs = os; bk = ok; }
         }
-        const int kstar = bk, own = kstar & 31, jst = kstar >> 5;
-        const double sstar = bs;
-        const double mstar = __shfl_sync(kFull, pick<S>(mg, jst), own);
+        kstar = bk;
+        own = kstar & 31;
+        jst = kstar >> 5;
+        sstar = bs;
+        mstar = __shfl_sync(kFull, pick<S>(mg, jst), own);
         const bool fresh_star = __shfl_sync(kFull, pick<S>(n, jst) == 0u, own);
 
         // ---- near-tie flag (ENV.md §4.5)
         bool tie = false;
-        double s2 = -kInf, m2 = 0.0;
 #pragma unroll
         for (int j = 0; j < S; ++j) {
             if (!((act >> j) & 1u) || (32 * j + lane) == kstar) continue;
@@ -222,21 +255,47 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
             if (sstar - sc[j] < a.tie_rel * sc_ && !(fresh_star && n[j] == 0u)) tie = true;
             if (sc[j] > s2) { s2 = sc[j]; m2 = mg[j]; }
         }
-        const bool near = __ballot_sync(kFull, tie) != 0u;
+        near = __ballot_sync(kFull, tie) != 0u;
+        if constexpr (MODE == 1) {                    // select ends here: nothing changes until observe
+            if (lane == 0) {
+                LivePend pd;
+#pragma unroll
+                for (int i = 0; i < 7; ++i) pd.x[i] = i < D ? x[i < D ? i : 0] : 0.0;
+                pd.kstar = (uint32_t)kstar;
+                pd.near = near ? 1u : 0u;
+                a.w.live[tb] = pd;
+                a.chosen[tb] = (uint32_t)kstar;
+            }
+            return;
+        }
+        }
 
         // ---- a7: ENV-R response at f = f_min + k*·step (ENV.md §3.3), exact arithmetic
+        double E, tpot, ttft, edp;
+        if constexpr (MODE == 2) {                    // live: the measured response, EDP = E·TPOT
+            const double *m = a.live_resp + tb * 3;
+            E = m[0];
+            tpot = m[1];
+            ttft = m[2];
+            edp = xmul(E, tpot);
+            if (!isfinite(E) || !isfinite(tpot) || !isfinite(ttft)) {
+                st.flags |= 1u;
+                break;
+            }
+        } else {
         const double dec = s_dec[kstar], pre = s_pre[kstar], pw = s_pw[kstar];
         const double t_dec = xmul((double)recI, dec);
         const double t_pre = xmul((double)recP, pre);
         const double busy = xmul(xadd(t_dec, t_pre), g);
         const double u = xmul(busy, invW);
         const double q = u <= a.u_max ? xdiv(1.0, xsub(1.0, u)) : xmul(u, q_over);
-        const double tpot = xmul(xmul(xmul(xadd(dec, xmul(t_pre, invIm)), g), q), nT);
+        tpot = xmul(xmul(xmul(xadd(dec, xmul(t_pre, invIm)), g), q), nT);
         double ue = u > 1.0 ? 1.0 : u;
         ue = ue < a.u_floor ? a.u_floor : ue;
-        const double E = xmul(xmul(xadd(a.p_idle, xmul(pw, ue)), a.W), nE);
-        const double ttft = xmul(xadd(xmul(t_pre, invAm), xmul(t_dec, wIm)), q);
-        const double edp = xmul(E, tpot);
+        E = xmul(xmul(xadd(a.p_idle, xmul(pw, ue)), a.W), nE);
+        ttft = xmul(xadd(xmul(t_pre, invAm), xmul(t_dec, wIm)), q);
+        edp = xmul(E, tpot);
+        }
 
         // ---- a8: reward = clip(1 − EDP/median(window)), then push EDP (AMB-3)
         double r = 0.0;
@@ -555,12 +614,12 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
     }
 }
 
-template <int D, int S>
+template <int D, int S, int MODE>
 static cudaError_t launch_ds(const ReplayArgs &a, cudaStream_t s)
 {
     constexpr int P = D * (D + 1) / 2;
     const size_t smem = (3 * kMaxArms + (size_t)kWarpsPerBlock * S * (P + D) * 32) * sizeof(double);
-    auto kern = replay_kernel<D, S>;
+    auto kern = replay_kernel<D, S, MODE>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const uint32_t blocks = (a.n_tuners + kWarpsPerBlock - 1) / kWarpsPerBlock;
@@ -568,30 +627,38 @@ static cudaError_t launch_ds(const ReplayArgs &a, cudaStream_t s)
     return cudaGetLastError();
 }
 
-template <int D>
+template <int D, int MODE>
 static cudaError_t launch_d(const ReplayArgs &a, cudaStream_t s)
 {
     const uint32_t slots = (a.K + 31) / 32;
     switch (slots) {
-    case 1: return launch_ds<D, 1>(a, s);
-    case 2: return launch_ds<D, 2>(a, s);
-    case 3: return launch_ds<D, 3>(a, s);
-    default: return launch_ds<D, 4>(a, s);
+    case 1: return launch_ds<D, 1, MODE>(a, s);
+    case 2: return launch_ds<D, 2, MODE>(a, s);
+    case 3: return launch_ds<D, 3, MODE>(a, s);
+    default: return launch_ds<D, 4, MODE>(a, s);
     }
 }
 
-cudaError_t launch_replay(const ReplayArgs &a, uint32_t D, cudaStream_t s)
+template <int MODE>
+static cudaError_t launch_mode(const ReplayArgs &a, uint32_t D, cudaStream_t s)
 {
     if (a.n_tuners == 0 || a.n_steps == 0) return cudaSuccess;
     switch (D) {
-    case 1: return launch_d<1>(a, s);
-    case 2: return launch_d<2>(a, s);
-    case 3: return launch_d<3>(a, s);
-    case 4: return launch_d<4>(a, s);
-    case 5: return launch_d<5>(a, s);
-    case 6: return launch_d<6>(a, s);
-    default: return launch_d<7>(a, s);
+    case 1: return launch_d<1, MODE>(a, s);
+    case 2: return launch_d<2, MODE>(a, s);
+    case 3: return launch_d<3, MODE>(a, s);
+    case 4: return launch_d<4, MODE>(a, s);
+    case 5: return launch_d<5, MODE>(a, s);
+    case 6: return launch_d<6, MODE>(a, s);
+    default: return launch_d<7, MODE>(a, s);
     }
+}
+
+cudaError_t launch_replay(const ReplayArgs &a, uint32_t D, cudaStream_t s) { return launch_mode<0>(a, D, s); }
+
+cudaError_t launch_live(const ReplayArgs &a, uint32_t D, int mode, cudaStream_t s)
+{
+    return mode == 1 ? launch_mode<1>(a, D, s) : launch_mode<2>(a, D, s);
 }
 
 }  // namespace agft

@@ -65,24 +65,8 @@ __global__ void __launch_bounds__(256) trace_kernel(const __grid_constant__ Trac
 
     // ---- ENV.md §3.2 record: context (§4.1) + row-only response terms
     StepRec rec;
-    double raw[7];
-    raw[0] = waiting > 0 ? 1.0 : 0.0;
-    raw[1] = xdiv((double)prefill, W);
-    raw[2] = xdiv((double)decode, W);
-    raw[3] = xdiv((double)((uint64_t)prefill + (uint64_t)decode), (double)(iters > 0 ? iters : 1u));
-    raw[4] = (double)running;
-    raw[5] = xdiv((double)kv_used, (double)c.kv_total);
-    raw[6] = (hits + misses) > 0 ? xdiv((double)hits, (double)(hits + misses)) : 0.0;
-#pragma unroll
-    for (int i = 0; i < 7; ++i) {
-        const double lo = a.norm_lo[i], hi = a.norm_hi[i];
-        double xv = 0.0;
-        if (hi > lo) {
-            xv = xdiv(xsub(raw[i], lo), xsub(hi, lo));
-            xv = xv < 0.0 ? 0.0 : (xv > 1.0 ? 1.0 : xv);
-        }
-        rec.x[i] = xv;
-    }
+    context_of(waiting, running, prefill, decode, iters, kv_used, hits, misses, W, c.kv_total, a.norm_lo,
+               a.norm_hi, rec.x);
     rec.I = iters;
     rec.P = prefill;
     const double rho = xdiv((double)(running + waiting), (double)a.cap);

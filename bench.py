@@ -146,8 +146,10 @@ def main():
     ap.add_argument("--scaling", default=None, choices=["weak", "strong"],
                     help="weak: every rank runs the full config (default for C1-C4); strong: split it (C5)")
     ap.add_argument("--backend", default="nccl", help="process-group backend for N > 1 (nccl; gloo for tests)")
-    ap.add_argument("--workload", default="replay", choices=["replay", "sweep"],
-                    help="replay: the tuner hot path (north-star metric); sweep: ENV.md §5 offline sweep")
+    ap.add_argument("--workload", default="replay", choices=["replay", "sweep", "live"],
+                    help="replay: the tuner hot path (north-star metric); sweep: ENV.md §5 offline sweep; "
+                         "live: agft_select/agft_observe decision latency")
+    ap.add_argument("--tuners", type=int, default=1024, help="live workload: tuners per GPU")
     args = ap.parse_args()
     if args.scaling is None:
         args.scaling = "strong" if args.config == "C5" else "weak"
@@ -170,6 +172,8 @@ def main():
         return reference_arm(args, cfg, rank, world)
     if args.workload == "sweep":
         return sweep_bench(args, cfg, rank, world, local)
+    if args.workload == "live":
+        return live_bench(args, cfg, rank, world, local)
 
     import numpy as np
     import torch
@@ -381,6 +385,130 @@ def sweep_bench(args, cfg, rank, world, local):
                      "oracle_le_fixed": bool(np.all(h["O"][:, 0][:, None] <= h["S"][:, :, 2]))}}
     if rank == 0:
         print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def live_bench(args, cfg, rank, world, local):
+    """Live two-phase step (agft_select → measured response → agft_observe):
+    one step = T windows for N tuners.  Device leg: snapshot rows and responses already in HBM
+    (the response of window t is a seeded measurement table, independent of the arm chosen);
+    e2e leg: every window copies the rows host→device, the chosen arms device→host (the
+    controller must set the clocks) and the measured responses host→device — the real loop."""
+    import torch
+    from agft_inputs import live_inputs, tuner_params
+    from paper_2508_01744_b200 import TunerBatch, _abi
+    torch.cuda.set_device(local % max(1, torch.cuda.device_count()))
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group(args.backend, device_id=torch.device("cuda", local)) if args.backend == "nccl" \
+            else dist.init_process_group(args.backend)
+    n = args.tuners
+    T = min(cfg["T"], args.T or 2000)
+    c = dict(cfg, n_tuners=n, n_traces=n, sweep="none")
+    params = tuner_params(c)
+    rows, resp = live_inputs(dict(c, n_arms=1), n, T, seed=17 + rank)      # one measurement per window
+    dev = torch.device("cuda", local % max(1, torch.cuda.device_count()))
+    rows_h = torch.from_numpy(np.ascontiguousarray(rows.transpose(1, 0, 2)).view(np.int32)).pin_memory()
+    resp_h = torch.from_numpy(np.ascontiguousarray(resp[:, :, 0, :].transpose(1, 0, 2))).pin_memory()
+    rows_d, resp_d = rows_h.to(dev), resp_h.to(dev)
+    tb = TunerBatch(c, params, device=dev)
+    stream = torch.cuda.current_stream()
+    chosen = torch.empty((T, n), dtype=torch.int32, device=dev)
+
+    def one(e2e=False):
+        tb.reset()
+        if not e2e:
+            for t in range(T):
+                tb.select(rows_d[t], chosen[t])
+                tb.observe(resp_d[t])
+            return None
+        r_buf = torch.empty((n, 12), dtype=torch.int32, device=dev)
+        m_buf = torch.empty((n, 3), dtype=torch.float64, device=dev)
+        ch_h = torch.empty(n, dtype=torch.int32).pin_memory()
+        for t in range(T):
+            r_buf.copy_(rows_h[t], non_blocking=True)
+            tb.select(r_buf, chosen[t])
+            ch_h.copy_(chosen[t], non_blocking=True)
+            torch.cuda.current_stream().synchronize()      # the controller applies the clocks here
+            m_buf.copy_(resp_h[t], non_blocking=True)
+            tb.observe(m_buf)
+        return None
+
+    for _ in range(args.warmup):
+        one()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    st0 = tb.stats()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = _abi.lib().agft_kernel_launches()
+    e0.record(stream)
+    for _ in range(args.steps):
+        one()
+    e1.record(stream)
+    launches = int(_abi.lib().agft_kernel_launches() - launches0)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    st = tb.stats()
+    k_act = float(st["sum_active"].astype(np.float64).sum())          # last step's Σ K_act
+    # e2e: host rows in, chosen arms out, host measurements in, every window
+    one(e2e=True)
+    torch.cuda.synchronize()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(args.steps):
+        one(e2e=True)
+    f1.record(stream)
+    torch.cuda.synchronize()
+    ms_e2e = f0.elapsed_time(f1)
+    if world > 1:
+        import torch.distributed as dist
+        t_ = torch.tensor([ms, ms_e2e], dtype=torch.float64, device="cuda" if args.backend == "nccl" else "cpu")
+        dist.all_reduce(t_, op=dist.ReduceOp.MAX)
+        ms, ms_e2e = float(t_[0]), float(t_[1])
+    decisions = float(n) * T * args.steps
+    pk = peaks()
+    sm_mhz = float(pk.get("sm_max_mhz", 1965.0))
+    peak_fp64 = N_SM * FP64_UNITS_PER_SM * 2 * sm_mhz * 1e6 / 1e12
+    d = c["d"]
+    P = d * (d + 1) // 2
+    # algorithmic HBM bytes (DESIGN.md §5, live): select reads the row (48), mask (16), stats (128),
+    # the scored arms' A⁻¹, θ, n ((P+d)·8 + 4 each) and writes the pending record (64) and k* (4);
+    # observe reads the measurement (24) and pending record (64), reads and writes the chosen arm's
+    # A⁻¹, θ, b and n, r̄, ē (2·((P+2d)·8 + 20)), reads n, r̄, ē of the active arms (20 each), and
+    # reads and writes the EDP window (2·1 KiB), the stats (2·128) and the mask (16)
+    per_dec = (48 + 16 + 128 + 64 + 4) + (24 + 64 + 2 * ((P + 2 * d) * 8 + 20) + 2 * 1024 + 2 * 128 + 16)
+    per_arm = (P + d) * 8 + 4 + 20
+    alg_bytes = (float(n) * T * per_dec + k_act * per_arm) * args.steps
+    achieved = alg_bytes / (ms / 1e3) / 1e9
+    peak_hbm = float(pk.get("hbm_gbs", 7700.0))
+    out = {"metric": "live decisions/s (agft_select + agft_observe, device-timed)",
+           "value": round(decisions * world / (ms / 1e3), 1), "unit": "tuner-decisions/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (agft_inputs.live_inputs snapshots + measurement table)",
+           "config": {"workload": f"live: {n} tuners × {c['n_arms']} arms × d={c['d']} × {T} windows",
+                      "tuners_per_gpu": n, "T": T, "us_per_window": round(ms * 1e3 / (T * args.steps), 2),
+                      "mean_active_arms": round(k_act / (float(n) * T), 3),
+                      "l2": "tuner state 80 KB/tuner: above L2 from ~1,500 tuners"},
+           "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": round(peak_hbm, 1),
+                        "unit": "GB/s", "frac": round(achieved / peak_hbm, 5), "traffic": None,
+                        "kernel": "replay_kernel<MODE 1|2> (the only launches of the step, besides one reset)",
+                        "algorithmic_bytes_per_decision": round(per_dec + per_arm * k_act / (float(n) * T), 1),
+                        "fp64_frac": round(flops_per_step(d, k_act, float(n) * T) * args.steps / (ms / 1e3) / 1e12
+                                           / peak_fp64, 6),
+                        "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"},
+           "clocks": clk, "gpu_launches": launches,
+           "e2e": {"value": round(decisions * world / (ms_e2e / 1e3), 1), "unit": "tuner-decisions/s",
+                   "h2d_bytes_per_step": n * T * (48 + 24), "d2h_bytes_per_step": n * T * 4,
+                   "us_per_window": round(ms_e2e * 1e3 / (T * args.steps), 2),
+                   "api": "agft_select/agft_observe with host rows/measurements in and chosen arms out each window"}}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    tb.close()
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()

@@ -141,21 +141,36 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
     uint32_t n[S];
     double rbar[S], ebar[S];
     uint32_t act = 0;                                 // bit j: arm 32j+lane active
+    // A single live window touches only what it needs (HBM-bound at large N): select reads the
+    // active arms' A⁻¹, θ and n; observe reads the chosen arm's A⁻¹, θ (all arms' when refinement
+    // may re-score them) plus n, r̄, ē for the pruning statistics, and writes back the chosen arm.
+    const uint32_t kpend = MODE == 2 ? a.w.live[tb].kstar : 0xFFFFFFFFu;
 #pragma unroll
     for (int j = 0; j < S; ++j) {
         const uint32_t k = 32u * j + lane;
+        const bool on = k < K && ((a.w.active[tb * 4 + j] >> lane) & 1u);
+        if (on) act |= 1u << j;
+        const bool ld = MODE == 0 || (MODE == 1 && on) || (MODE == 2 && (a.rf_enable || k == kpend));
+        if (ld) {
 #pragma unroll
-        for (int e = 0; e < P; ++e) sA[(j * P + e) * 32 + lane] = a.w.ainv[(tb * P + e) * kMaxArms + k];
+            for (int e = 0; e < P; ++e) sA[(j * P + e) * 32 + lane] = a.w.ainv[(tb * P + e) * kMaxArms + k];
 #pragma unroll
-        for (int i = 0; i < D; ++i) sT[(j * D + i) * 32 + lane] = a.w.theta[(tb * D + i) * kMaxArms + k];
-        n[j] = a.w.n[tb * kMaxArms + k];
-        rbar[j] = a.w.rbar[tb * kMaxArms + k];
-        ebar[j] = a.w.ebar[tb * kMaxArms + k];
-        if (k < K && ((a.w.active[tb * 4 + j] >> lane) & 1u)) act |= 1u << j;
+            for (int i = 0; i < D; ++i) sT[(j * D + i) * 32 + lane] = a.w.theta[(tb * D + i) * kMaxArms + k];
+        }
+        n[j] = (MODE != 1 || on) ? a.w.n[tb * kMaxArms + k] : 0u;
+        rbar[j] = MODE != 1 ? a.w.rbar[tb * kMaxArms + k] : 0.0;
+        ebar[j] = MODE != 1 ? a.w.ebar[tb * kMaxArms + k] : 0.0;
     }
-    double wlo = a.w.wsorted[tb * kWindow + 2 * lane], whi = a.w.wsorted[tb * kWindow + 2 * lane + 1];
-    double rlo = a.w.wring[tb * kWindow + 2 * lane], rhi = a.w.wring[tb * kWindow + 2 * lane + 1];
-    uint32_t wcount = a.w.wmeta[tb * 2], whead = a.w.wmeta[tb * 2 + 1];
+    double wlo = 0.0, whi = 0.0, rlo = 0.0, rhi = 0.0;
+    uint32_t wcount = 0u, whead = 0u;
+    if (MODE != 1) {                                  // select never touches the EDP window
+        wlo = a.w.wsorted[tb * kWindow + 2 * lane];
+        whi = a.w.wsorted[tb * kWindow + 2 * lane + 1];
+        rlo = a.w.wring[tb * kWindow + 2 * lane];
+        rhi = a.w.wring[tb * kWindow + 2 * lane + 1];
+        wcount = a.w.wmeta[tb * 2];
+        whead = a.w.wmeta[tb * 2 + 1];
+    }
     const uint32_t M = a.median_window;
 
     const StepRec *rp = a.records + (size_t)prm.trace_id * a.rec_stride + a.rec_off;
@@ -578,13 +593,15 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
 #pragma unroll
     for (int j = 0; j < S; ++j) {
         const uint32_t k = 32u * j + lane;
+        if (MODE == 0 || k == kpend) {                // a live window changed only the chosen arm
 #pragma unroll
-        for (int e = 0; e < P; ++e) a.w.ainv[(tb * P + e) * kMaxArms + k] = sA[(j * P + e) * 32 + lane];
+            for (int e = 0; e < P; ++e) a.w.ainv[(tb * P + e) * kMaxArms + k] = sA[(j * P + e) * 32 + lane];
 #pragma unroll
-        for (int i = 0; i < D; ++i) a.w.theta[(tb * D + i) * kMaxArms + k] = sT[(j * D + i) * 32 + lane];
-        a.w.n[tb * kMaxArms + k] = n[j];
-        a.w.rbar[tb * kMaxArms + k] = rbar[j];
-        a.w.ebar[tb * kMaxArms + k] = ebar[j];
+            for (int i = 0; i < D; ++i) a.w.theta[(tb * D + i) * kMaxArms + k] = sT[(j * D + i) * 32 + lane];
+            a.w.n[tb * kMaxArms + k] = n[j];
+            a.w.rbar[tb * kMaxArms + k] = rbar[j];
+            a.w.ebar[tb * kMaxArms + k] = ebar[j];
+        }
         const uint32_t bits = __ballot_sync(kFull, (act >> j) & 1u);
         if (lane == 0) a.w.active[tb * 4 + j] = bits;
     }

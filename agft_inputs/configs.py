@@ -46,6 +46,8 @@ _BASE = {
     # mixed maturity-based refinement (ENV.md §4.11): off in C1–C5
     "rf_enable": 0, "rf_period": 25, "rf_mature": 100, "rf_min_samples": 4, "rf_half_mhz": 150,
     "rf_step_mhz": 15,
+    # ENV-C closed loop (ENV.md §6): off in C1–C5; backlog cap 4·cap
+    "cl_enable": 0, "cl_q_max": 256,
     # pruning
     "prune_enable": 1, "ext_round_limit": 60, "ext_min_samples": 3, "ext_reward_threshold": -1.2,
     "hist_min_round": 30, "hist_min_samples": 6, "hist_k": 1.0, "cascade_fraction": 0.5,

@@ -52,6 +52,7 @@ class OrcConfig(C.Structure):
         ("ph_enable", u32), ("ph_window", u32), ("ph_delta", f64), ("ph_lambda", f64),
         ("rf_enable", u32), ("rf_period", u32), ("rf_mature", u32), ("rf_min_samples", u32),
         ("rf_half_mhz", u32), ("rf_step_mhz", u32),
+        ("cl_enable", u32), ("cl_q_max", u32),
     ]
 
 
@@ -91,7 +92,7 @@ class OrcRecord(C.Structure):
                 ("reward", C.POINTER(f64)), ("edp", C.POINTER(f64)), ("energy", C.POINTER(f64)),
                 ("tpot", C.POINTER(f64)), ("ttft", C.POINTER(f64)), ("scores", C.POINTER(f64)),
                 ("x", C.POINTER(f64)), ("n_active", C.POINTER(u32)),
-                ("active_mask", C.POINTER(u32))]
+                ("active_mask", C.POINTER(u32)), ("backlog", C.POINTER(u32))]
 
 
 class OrcInject(C.Structure):
@@ -114,6 +115,8 @@ def lib():
         L.orc_trace_rows.argtypes = [C.POINTER(OrcConfig), u32, u32, u32, C.POINTER(u32)]
         L.orc_context.argtypes = [C.POINTER(OrcConfig), C.POINTER(u32), C.POINTER(f64)]
         L.orc_env_response.argtypes = [C.POINTER(OrcConfig), C.POINTER(u32), u32, C.POINTER(f64)]
+        L.orc_closed_next.argtypes = [C.POINTER(OrcConfig), C.POINTER(u32), u32, u32]
+        L.orc_closed_next.restype = u32
         L.orc_step_record.argtypes = [C.POINTER(OrcConfig), C.POINTER(u32), C.POINTER(OrcStepRec)]
         L.orc_response.argtypes = [C.POINTER(OrcConfig), C.POINTER(OrcStepRec), u32, C.POINTER(f64)]
         L.orc_median.argtypes = [C.POINTER(f64), u32]
@@ -225,6 +228,13 @@ def context(cfg: dict, row) -> np.ndarray:
     return x
 
 
+def closed_next(cfg: dict, row, q: int, f_mhz: int) -> int:
+    """ENV.md §6: backlog carried out of a window (row without the carried-in q) run at f_mhz."""
+    oc = make_config(cfg)
+    r = np.ascontiguousarray(row, dtype=np.uint32)
+    return int(lib().orc_closed_next(C.byref(oc), _ptr(r, u32), int(q), int(f_mhz)))
+
+
 def env_response(cfg: dict, row, f_mhz: int):
     oc = make_config(cfg)
     r = np.ascontiguousarray(row, dtype=np.uint32)
@@ -326,14 +336,15 @@ def run_tuner(cfg: dict, tuner: OrcTuner | None = None, T: int | None = None, fo
         recd = {"arm": np.zeros(T, np.uint8), "near_tie": np.zeros(T, np.uint8),
                 "reward": np.zeros(T), "edp": np.zeros(T), "energy": np.zeros(T),
                 "tpot": np.zeros(T), "ttft": np.zeros(T), "x": np.zeros((T, d)),
-                "n_active": np.zeros(T, np.uint32), "active_mask": np.zeros((T, 4), np.uint32)}
+                "n_active": np.zeros(T, np.uint32), "active_mask": np.zeros((T, 4), np.uint32),
+                "backlog": np.zeros(T, np.uint32)}
         if scores:
             recd["scores"] = np.zeros((T, K))
         rec = OrcRecord()
         for name, ct in OrcRecord._fields_:
             if name in recd:
                 base = {"arm": C.c_uint8, "near_tie": C.c_uint8, "n_active": u32,
-                        "active_mask": u32}.get(name, f64)
+                        "active_mask": u32, "backlog": u32}.get(name, f64)
                 setattr(rec, name, _ptr(recd[name], base))
         rec_p = C.byref(rec)
     inj_p = None

@@ -449,6 +449,32 @@ double orc_reward(double edp, const double *window, uint32_t n, double clip_lo, 
     return r;
 }
 
+/* ENV.md §6 (ENV-C): requests the server running window `row` at F leaves queued for the next
+ * window.  The window's utilisation u is §3.3's (busy / W) on the record of the row with the
+ * carried-in backlog added to `waiting`; a window that needs u > 1 windows of work serves only
+ * floor(D / u) of its D = arrivals + backlog requests (the rest keep waiting). */
+static uint32_t closed_next(const orc_config *c, const orc_steprec *rec, uint32_t a, uint32_t q, uint32_t F)
+{
+    double dec, pre, pw;
+    freq_consts(c, F, &dec, &pre, &pw);
+    double invW = 1.0 / c->W;
+    double u = ((((double)rec->I * dec) + ((double)rec->P * pre)) * rec->g) * invW;
+    uint32_t D = a + q;
+    uint32_t served = u > 1.0 ? (uint32_t)floor((double)D / u) : D;
+    uint32_t left = D - served;
+    return left < c->cl_q_max ? left : c->cl_q_max;
+}
+
+uint32_t orc_closed_next(const orc_config *c, const uint32_t row[ORC_ROW_WORDS], uint32_t q, uint32_t F)
+{
+    uint32_t rq[ORC_ROW_WORDS];
+    memcpy(rq, row, sizeof(rq));
+    rq[0] = row[0] + q;
+    orc_steprec rec;
+    orc_step_record(c, rq, &rec);
+    return closed_next(c, &rec, row[6] + row[7], q, F);
+}
+
 int orc_run_tuner(const orc_config *c, const orc_tuner *tu, uint32_t T, const uint8_t *follow,
                   orc_stats *st, orc_arms *arms_out, const orc_record *rec)
 {
@@ -479,7 +505,8 @@ int orc_run_tuner_ex(const orc_config *c, const orc_tuner *tu, uint32_t T, const
 
     /* f_max baseline response constants are folded into orc_env_response */
     uint32_t row[ORC_ROW_WORDS];
-    orc_steprec srec;
+    orc_steprec srec, srecb;
+    uint32_t cl_q = 0, cl_qb = 0;                                    /* ENV-C backlogs (§6) */
     double x[7];
     double s[ORC_MAX_ARMS], mag[ORC_MAX_ARMS];
 
@@ -495,7 +522,19 @@ int orc_run_tuner_ex(const orc_config *c, const orc_tuner *tu, uint32_t T, const
             }
         } else {
             orc_trace_row(c, tu->trace_id, t, row);                  /* a0 */
-            orc_step_record(c, row, &srec);                          /* a2 + the row-only part of a7 */
+            if (c->cl_enable) {                                      /* §6: the servers see their backlog */
+                uint32_t rq[ORC_ROW_WORDS], rb[ORC_ROW_WORDS];
+                memcpy(rq, row, sizeof(rq));
+                memcpy(rb, row, sizeof(rb));
+                rq[0] = row[0] + cl_q;
+                rb[0] = row[0] + cl_qb;
+                orc_step_record(c, rq, &srec);
+                orc_step_record(c, rb, &srecb);
+                srec.baseE = srecb.baseE;                            /* baseline = the f_max server */
+                srec.baseEDP = srecb.baseEDP;
+            } else {
+                orc_step_record(c, row, &srec);                      /* a2 + the row-only part of a7 */
+            }
             for (uint32_t i = 0; i < 7; ++i) x[i] = srec.x[i];
         }
         double alpha = tu->alpha0 / sqrt(1.0 + (double)t / c->tau);   /* a3, AMB-1 */
@@ -569,6 +608,12 @@ int orc_run_tuner_ex(const orc_config *c, const orc_tuner *tu, uint32_t T, const
             orc_response(c, &srec, F, resp);
         }
         double E = resp[0], tpot = resp[1], ttft = resp[2], edp = resp[3];
+        if (!inj && c->cl_enable) {                                   /* §6: backlog into window t+1 */
+            const uint32_t a = row[6] + row[7];
+            cl_q = closed_next(c, &srec, a, cl_q, F);
+            cl_qb = closed_next(c, &srecb, a, cl_qb, c->f_max_hw_mhz);
+        }
+        if (rec && rec->backlog) rec->backlog[t] = cl_q;
         double r = orc_reward(edp, S->window, S->wcount, c->clip_lo, c->clip_hi);
         if (inj && inj->reward) r = inj->reward[(size_t)t * K + kstar];
         const uint32_t phase_sel = S->phase;

@@ -49,6 +49,8 @@ typedef struct {
     uint32_t rf_enable, rf_period;     /* on/off; evaluated every rf_period rounds (25) */
     uint32_t rf_mature, rf_min_samples;/* t_mature (100); statistical anchor needs n ≥ 4 */
     uint32_t rf_half_mhz, rf_step_mhz; /* window ±150 MHz, step 15 MHz */
+    /* ENV-C closed loop (ENV.md §6) */
+    uint32_t cl_enable, cl_q_max;      /* on/off; backlog cap (requests) */
 } orc_config;
 
 typedef struct {                       /* per-tuner hyper-parameters (the sweep axes) */
@@ -96,6 +98,7 @@ typedef struct {                       /* optional per-step record (any pointer 
     double *x;                         /* [T][d] */
     uint32_t *n_active;                /* [T] after pruning */
     uint32_t *active_mask;             /* [T][4] after pruning (caller zeroes it) */
+    uint32_t *backlog;                 /* [T] ENV-C q carried out of window t (§6) */
 } orc_record;
 
 typedef struct {                       /* unit-test / live environment: replaces ENV-T/ENV-R */
@@ -148,6 +151,10 @@ uint32_t orc_argmin(const double *v, uint32_t K, uint32_t stride);
  * refined action space around an anchor (window minus extreme-pruned arms). */
 uint32_t orc_stat_anchor(const orc_config *c, const uint32_t *n, const double *ebar, const uint8_t *extreme);
 uint32_t orc_refine_window(const orc_config *c, uint32_t anchor, const uint8_t *extreme, uint8_t *active_out);
+
+/* ENV.md §6: the backlog carried out of a window with snapshot `row` (waiting NOT yet including
+ * the carried-in backlog q) run at F MHz: q' = min(q_max, D - served), D = arrivals + q. */
+uint32_t orc_closed_next(const orc_config *c, const uint32_t row[ORC_ROW_WORDS], uint32_t q, uint32_t F_mhz);
 
 uint32_t orc_sizeof(int which /* 0 config 1 tuner 2 stats 3 arms 4 steprec 5 record 6 inject */);
 

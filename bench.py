@@ -136,6 +136,8 @@ def main():
     ap.add_argument("--T", type=int, default=None, help="override decision windows (debug only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--closed", action="store_true",
+                    help="ENV-C closed-loop environment (ENV.md §6; WIDE schedule, raw rows alongside the records)")
     ap.add_argument("--refine", action="store_true",
                     help="enable mixed maturity-based refinement (ENV.md §4.11; WIDE schedule)")
     ap.add_argument("--chunk", type=int, default=CHUNK, help="windows per agft_replay call (records buffer)")
@@ -166,6 +168,8 @@ def main():
         cfg["ph_enable"] = 1          # ENV.md §4.10 exploitation phase
     if args.refine:
         cfg["rf_enable"] = 1          # ENV.md §4.11 refinement (NEXT row 1; WIDE schedule)
+    if args.closed:
+        cfg["cl_enable"] = 1          # ENV.md §6 closed loop (NEXT row 3; WIDE schedule)
     T = cfg["T"]
 
     if args.impl == "reference":
@@ -199,6 +203,8 @@ def main():
     stream = torch.cuda.current_stream()
     chunk = min(args.chunk, T)
     records = tb.new_records(chunk)
+    raw = (torch.empty((R, chunk, pkg.ROW_WORDS), dtype=torch.int32, device=f"cuda:{local}")
+           if args.closed else None)
     stats_out = tb.stats_tensor()
     coll_dev = stats_out.device if args.backend == "nccl" else torch.device("cpu")
     gathered = (torch.empty(world * stats_out.numel(), dtype=torch.uint8, device=coll_dev)
@@ -211,15 +217,15 @@ def main():
         t = 0
         while t < T:
             m = min(chunk, T - t)
-            tb.generate(t, m, records)
+            pkg.agft_trace_generate(tb.h, t, m, records, raw)
             if timed:
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
-                tb.replay(records, t, m)
+                tb.replay(records, t, m, raw=raw)
                 e1.record(stream)
                 ev_replay.append((e0, e1))
             else:
-                tb.replay(records, t, m)
+                tb.replay(records, t, m, raw=raw)
             t += m
         pkg.agft_stats(tb.h, stats_out)
         if world > 1:
@@ -283,6 +289,7 @@ def main():
                       "tuners_per_gpu": n, "T": T, "arms": cfg["n_arms"], "d": cfg["d"],
                       "phase_switch": bool(cfg.get("ph_enable", 0)),
                       "refinement": bool(cfg.get("rf_enable", 0)),
+                      "closed_loop": bool(cfg.get("cl_enable", 0)),
                       "traces_per_gpu": R, "chunk": chunk,
                       "l2": f"inputs larger than L2: tuner state {tb.workspace.numel() / 2**30:.2f} GiB/GPU",
                       "parallelism": f"tuner shards dp{world}"},
@@ -525,7 +532,8 @@ def e2e_leg(cfg, params, trace_base, world, local, chunk, n, T, args) -> dict:
     cfg_c = make_config(cfg, n_tuners=n, n_traces=cfg["n_traces"], trace_base=trace_base,
                         policy=args.policy)
     ws = torch.empty(pkg.agft_workspace_bytes(cfg_c), dtype=torch.uint8, device=dev)
-    scratch = torch.empty(cfg["n_traces"] * chunk * pkg.RECORD_BYTES, dtype=torch.uint8, device=dev)
+    per = pkg.RECORD_BYTES + (pkg.ROW_WORDS * 4 if cfg.get("cl_enable") else 0)   # + raw rows (ENV.md §6)
+    scratch = torch.empty(cfg["n_traces"] * chunk * per, dtype=torch.uint8, device=dev)
     hp = torch.from_numpy(make_params(params).view(np.uint8)).pin_memory()
     dp = torch.empty_like(hp, device=dev)
     ds = torch.empty(n * STATS_DTYPE.itemsize, dtype=torch.uint8, device=dev)

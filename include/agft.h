@@ -30,7 +30,8 @@
 extern "C" {
 #endif
 
-#define AGFT_ABI_VERSION 4u         /* 2: + agft_phase; 3: + agft_refine (and their stats); 4: + agft_select/agft_observe */
+#define AGFT_ABI_VERSION 5u         /* 2: + agft_phase; 3: + agft_refine (and their stats); 4: + agft_select/agft_observe;
+                                       5: + agft_closed / agft_replay_raw */
 #define AGFT_MAX_ARMS 128u          /* K ≤ 128 */
 #define AGFT_MAX_D 7u               /* the paper's 7-dim context */
 #define AGFT_MAX_WINDOW 64u         /* reward-median window, AMB-3 */
@@ -99,6 +100,12 @@ typedef struct { uint32_t enable, window; double delta, lambda; } agft_phase;
  * t < mature, the UCB argmax after — minus Extreme-pruned arms.  Runs on the WIDE schedule. */
 typedef struct { uint32_t enable, period, mature, min_samples, half_mhz, step_mhz; } agft_refine;
 
+/* ENV-C closed loop (ENV.md §6): requests a window cannot
+ * serve at the chosen clock (u > 1) wait into the next window, where the snapshot sees them
+ * (x1, the concurrency penalty, TTFT); the f_max baseline carries its own backlog.  q_max caps
+ * the backlog (requests).  Needs the raw rows: replay with agft_replay_raw.  WIDE schedule. */
+typedef struct { uint32_t enable, q_max; } agft_closed;
+
 typedef struct {
     uint32_t abi_version;     /* must be AGFT_ABI_VERSION */
     uint32_t n_tuners;        /* N ≥ 1 */
@@ -118,6 +125,7 @@ typedef struct {
     agft_phase phase;                /* Page-Hinkley exploitation switch (ENV.md §4.10) */
     agft_refine refine;              /* mixed maturity-based refinement (ENV.md §4.11) */
     uint32_t pad1;
+    agft_closed closed;              /* ENV-C closed loop (ENV.md §6) */
 } agft_config;
 
 /* Per-tuner parameters (the hyper-parameter sweep axes of C4/C5). */
@@ -209,6 +217,13 @@ agft_status agft_observe(agft_handle h, const double *d_resp);
 agft_status agft_replay(agft_handle h, const void *d_records, uint32_t t0, uint32_t n_steps,
                         uint8_t *d_traj, double *d_gap);
 
+/* agft_replay with the raw ENV-T rows of the same windows alongside: d_raw = [n_traces][n_steps][12]
+ * uint32 as agft_trace_generate writes them.  Required when closed.enable (ENV-C reads arrivals,
+ * running and waiting from the rows); otherwise identical to agft_replay.  agft_replay, agft_step,
+ * agft_select and agft_observe return AGFT_E_INVALID_ARG on a closed-loop handle. */
+agft_status agft_replay_raw(agft_handle h, const void *d_records, const uint32_t *d_raw, uint32_t t0,
+                            uint32_t n_steps, uint8_t *d_traj, double *d_gap);
+
 /* Copy the per-tuner statistics into d_out [n_tuners]. */
 agft_status agft_stats(agft_handle h, agft_tuner_stats *d_out);
 
@@ -224,7 +239,8 @@ agft_status agft_get_step(agft_handle h, uint32_t *t);
 
 /* End to end from HOST buffers: copies h_params [n_tuners] host→device, creates the
  * tuners in d_workspace, replays steps [0, n_steps) generating the trace in chunks of
- * chunk_steps into d_scratch (≥ n_traces·chunk_steps·128 B), and copies the statistics
+ * chunk_steps into d_scratch (≥ n_traces·chunk_steps·128 B; ·176 B with closed.enable, the raw
+ * rows following the records), and copies the statistics
  * device→host into h_stats [n_tuners].  d_params_buf is a device buffer of n_tuners
  * agft_tuner_params and d_stats_buf of n_tuners agft_tuner_stats.  Synchronises. */
 agft_status agft_run(const agft_config *cfg, const agft_tuner_params *h_params,

@@ -19,7 +19,7 @@ from ._abi import (NO_RECORD, PARAMS_DTYPE, RECORD_BYTES, ROW_WORDS, STATS_DTYPE
                    make_config, make_params)
 
 __all__ = ["agft_workspace_bytes", "agft_create", "agft_reset", "agft_trace_generate", "agft_step", "agft_replay",
-           "agft_select", "agft_observe",
+           "agft_select", "agft_observe", "agft_replay_raw",
            "agft_stats", "agft_export_arms", "agft_get_step", "agft_run", "agft_sweep", "agft_regret",
            "agft_destroy", "SweepSums",
            "TunerBatch", "record_slot_count", "make_config", "make_params", "PARAMS_DTYPE", "STATS_DTYPE", "NO_RECORD",
@@ -80,6 +80,11 @@ def agft_observe(h, resp):
 
 def agft_replay(h, records, t0, n_steps, traj=None, gap=None):
     _abi.check("agft_replay", _abi.lib().agft_replay(h, _p(records), t0, n_steps, _p(traj), _p(gap)))
+
+
+def agft_replay_raw(h, records, raw, t0, n_steps, traj=None, gap=None):
+    _abi.check("agft_replay_raw", _abi.lib().agft_replay_raw(h, _p(records), _p(raw), t0, n_steps, _p(traj),
+                                                              _p(gap)))
 
 
 def agft_stats(h, out):
@@ -185,13 +190,21 @@ class TunerBatch:
         agft_trace_generate(self.h, t0, n_steps, records, rawt)
         return (records, rawt) if raw else records
 
-    def replay(self, records, t0: int, n_steps: int, record: bool = False):
+    @property
+    def closed(self) -> bool:
+        """ENV-C closed loop (ENV.md §6): replays need the raw rows (agft_replay_raw)."""
+        return bool(self.cfg.get("cl_enable", 0))
+
+    def replay(self, records, t0: int, n_steps: int, record: bool = False, raw=None):
         import torch
         traj = gap = None
         if record and self.record_slots:
             traj = torch.zeros((self.record_slots, n_steps), dtype=torch.uint8, device=self.device)
             gap = torch.zeros((self.record_slots, n_steps), dtype=torch.float64, device=self.device)
-        agft_replay(self.h, records, t0, n_steps, traj, gap)
+        if raw is not None:
+            agft_replay_raw(self.h, records, raw, t0, n_steps, traj, gap)
+        else:
+            agft_replay(self.h, records, t0, n_steps, traj, gap)
         return traj, gap
 
     def step(self, records_t):
@@ -218,14 +231,16 @@ class TunerBatch:
         """Generate + replay steps [t, T) in chunks; returns recorded traj/gap (host) if asked."""
         import torch
         trajs, gaps = [], []
-        rec = None
+        rec = raw = None
         t = self.t
         while t < T:
             n = min(chunk, T - t)
             if rec is None or rec.shape[1] != n:
                 rec = self.new_records(n)
-            self.generate(t, n, rec)
-            tr, gp = self.replay(rec, t, n, record=record)
+                raw = (torch.empty((self.n_traces, n, ROW_WORDS), dtype=torch.int32, device=self.device)
+                       if self.closed else None)
+            agft_trace_generate(self.h, t, n, rec, raw)
+            tr, gp = self.replay(rec, t, n, record=record, raw=raw)
             if record and tr is not None:
                 trajs.append(tr.cpu())
                 gaps.append(gp.cpu())

@@ -14,7 +14,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("AGFT_LIB_PATH") or os.path.join(HERE, "libagft.so")   # override: A/B builds
 
-ABI_VERSION = 4
+ABI_VERSION = 5
 RECORD_BYTES = 128
 ROW_WORDS = 12
 NO_RECORD = 0xFFFFFFFF
@@ -62,12 +62,16 @@ class AgftRefine(C.Structure):
                 ("half_mhz", u32), ("step_mhz", u32)]
 
 
+class AgftClosed(C.Structure):
+    _fields_ = [("enable", u32), ("q_max", u32)]
+
+
 class AgftConfig(C.Structure):
     _fields_ = [("abi_version", u32), ("n_tuners", u32), ("d", u32), ("n_traces", u32),
                 ("trace_base", u32), ("record_slots", u32), ("kernel_policy", u32), ("pad0", u32),
                 ("grid", AgftGrid), ("prune", AgftPrune), ("policy", AgftPolicy), ("env", AgftEnv),
                 ("trace", AgftTraceCfg), ("norm_lo", f64 * 7), ("norm_hi", f64 * 7), ("env_seed", u64),
-                ("phase", AgftPhase), ("refine", AgftRefine), ("pad1", u32)]
+                ("phase", AgftPhase), ("refine", AgftRefine), ("pad1", u32), ("closed", AgftClosed)]
 
 
 PARAMS_DTYPE = np.dtype([("trace_id", "<u4"), ("record_slot", "<u4"), ("alpha0", "<f8"),
@@ -100,6 +104,7 @@ PROTOTYPES = {
     "agft_select": (C.c_int, [vp, vp, vp]),
     "agft_observe": (C.c_int, [vp, vp]),
     "agft_replay": (C.c_int, [vp, vp, u32, u32, vp, vp]),
+    "agft_replay_raw": (C.c_int, [vp, vp, vp, u32, u32, vp, vp]),
     "agft_stats": (C.c_int, [vp, vp]),
     "agft_export_arms": (C.c_int, [vp, u32, vp, vp, vp, vp, vp, vp, vp]),
     "agft_get_step": (C.c_int, [vp, C.POINTER(u32)]),
@@ -181,6 +186,7 @@ def make_config(cfg: dict, n_tuners: int | None = None, n_traces: int | None = N
                         cfg.get("ph_lambda", 0.25))
     c.refine = AgftRefine(cfg.get("rf_enable", 0), cfg.get("rf_period", 25), cfg.get("rf_mature", 100),
                           cfg.get("rf_min_samples", 4), cfg.get("rf_half_mhz", 150), cfg.get("rf_step_mhz", 15))
+    c.closed = AgftClosed(cfg.get("cl_enable", 0), cfg.get("cl_q_max", 256))
     return c
 
 

@@ -126,6 +126,7 @@ agft_status validate(const agft_config *c)
     const agft_refine &rf = c->refine;               // ENV.md §4.11
     if (rf.enable > 1u) return AGFT_E_INVALID_ARG;
     if (rf.enable && (rf.period < 1u || rf.step_mhz < 1u)) return AGFT_E_INVALID_ARG;
+    if (c->closed.enable > 1u) return AGFT_E_INVALID_ARG;   // ENV.md §6
     const agft_phase &ph = c->phase;                 // ENV.md §4.10
     if (ph.enable > 1u) return AGFT_E_INVALID_ARG;
     if (ph.enable && (ph.window < 1u || !finite(ph.delta) || !finite(ph.lambda) || ph.delta < 0 || ph.lambda < 0))
@@ -213,6 +214,9 @@ ReplayArgs replay_args(agft_handle h, const void *records, uint32_t t0, uint32_t
     a.u_floor = c.env.u_floor;
     a.u_max = c.env.u_max;
     a.kv_total = c.trace.kv_total;
+    a.cl_enable = c.closed.enable;
+    a.cl_q_max = c.closed.q_max;
+    a.cap = c.trace.cap;
     std::memcpy(a.norm_lo, c.norm_lo, sizeof(a.norm_lo));
     std::memcpy(a.norm_hi, c.norm_hi, sizeof(a.norm_hi));
     return a;
@@ -345,7 +349,7 @@ agft_status agft_trace_generate(agft_handle h, uint32_t t0, uint32_t n_steps, vo
 // The replay scheduler: steps [t0, t0+n) in sub-chunks; before each sub-chunk every tuner
 // is classified by its active-arm count and each class runs its kernel on its own stream.
 static agft_status run_steps(agft_handle h, const void *d_records, uint32_t t0, uint32_t n, uint8_t *traj,
-                             double *gap, uint32_t *chosen)
+                             double *gap, uint32_t *chosen, const uint32_t *raw = nullptr)
 {
     const agft_config &c = h->cfg;
     for (uint32_t s = 0; s < n;) {
@@ -359,9 +363,11 @@ static agft_status run_steps(agft_handle h, const void *d_records, uint32_t t0, 
         a.traj = c.record_slots ? traj : nullptr;
         a.gap = c.record_slots ? gap : nullptr;
         a.chosen = chosen;
+        a.raw = raw;
         cudaError_t e = cudaSuccess;
-        // refinement re-admits arms, so a tuner's class can grow: one warp per tuner throughout
-        if (c.kernel_policy == AGFT_POLICY_WIDE || c.refine.enable) {
+        // refinement re-admits arms, so a tuner's class can grow: one warp per tuner throughout;
+        // the closed loop (ENV.md §6) is implemented on the WIDE mapping only
+        if (c.kernel_policy == AGFT_POLICY_WIDE || c.refine.enable || c.closed.enable) {
             e = launch_replay(a, c.d, h->stream);
         } else {
             // MSEG and LANE do not implement the exploitation phase (ENV.md §4.10): AUTO instead
@@ -400,9 +406,22 @@ agft_status agft_replay(agft_handle h, const void *d_records, uint32_t t0, uint3
 {
     if (!h || !d_records) return AGFT_E_INVALID_ARG;
     if (h->sticky != AGFT_OK) return h->sticky;
+    if (h->cfg.closed.enable) return AGFT_E_INVALID_ARG;     // needs the raw rows: agft_replay_raw
     if (t0 != h->t || h->live_pending) return AGFT_E_STATE;
     if (n_steps == 0) return AGFT_OK;
     agft_status st = run_steps(h, d_records, t0, n_steps, d_traj, d_gap, nullptr);
+    if (st == AGFT_OK) h->t += n_steps;
+    return st;
+}
+
+agft_status agft_replay_raw(agft_handle h, const void *d_records, const uint32_t *d_raw, uint32_t t0,
+                            uint32_t n_steps, uint8_t *d_traj, double *d_gap)
+{
+    if (!h || !d_records || !d_raw) return AGFT_E_INVALID_ARG;
+    if (h->sticky != AGFT_OK) return h->sticky;
+    if (t0 != h->t || h->live_pending) return AGFT_E_STATE;
+    if (n_steps == 0) return AGFT_OK;
+    agft_status st = run_steps(h, d_records, t0, n_steps, d_traj, d_gap, nullptr, d_raw);
     if (st == AGFT_OK) h->t += n_steps;
     return st;
 }
@@ -411,6 +430,7 @@ agft_status agft_step(agft_handle h, const void *d_records, uint32_t *d_chosen)
 {
     if (!h || !d_records) return AGFT_E_INVALID_ARG;
     if (h->sticky != AGFT_OK) return h->sticky;
+    if (h->cfg.closed.enable) return AGFT_E_INVALID_ARG;
     if (h->live_pending) return AGFT_E_STATE;
     agft_status st = run_steps(h, d_records, h->t, 1, nullptr, nullptr, d_chosen);
     if (st == AGFT_OK) h->t += 1;
@@ -422,6 +442,7 @@ agft_status agft_select(agft_handle h, const uint32_t *d_rows, uint32_t *d_chose
 {
     if (!h || !d_rows || !d_chosen) return AGFT_E_INVALID_ARG;
     if (reinterpret_cast<uintptr_t>(d_rows) % 16 != 0) return AGFT_E_INVALID_ARG;
+    if (h->cfg.closed.enable) return AGFT_E_INVALID_ARG;     // a live server is closed-loop by itself
     if (h->sticky != AGFT_OK) return h->sticky;
     if (h->live_pending) return AGFT_E_STATE;
     ReplayArgs a = replay_args(h, nullptr, h->t, 1);
@@ -435,6 +456,7 @@ agft_status agft_select(agft_handle h, const uint32_t *d_rows, uint32_t *d_chose
 agft_status agft_observe(agft_handle h, const double *d_resp)
 {
     if (!h || !d_resp) return AGFT_E_INVALID_ARG;
+    if (h->cfg.closed.enable) return AGFT_E_INVALID_ARG;
     if (h->sticky != AGFT_OK) return h->sticky;
     if (!h->live_pending) return AGFT_E_STATE;
     ReplayArgs a = replay_args(h, nullptr, h->t, 1);
@@ -500,7 +522,11 @@ agft_status agft_run(const agft_config *cfg, const agft_tuner_params *h_params, 
     if (st != AGFT_OK) return st;
     if (!h_params || !d_params_buf || !d_scratch || !d_stats_buf || !h_stats || chunk_steps == 0)
         return AGFT_E_INVALID_ARG;
-    if (scratch_bytes < (size_t)cfg->n_traces * chunk_steps * AGFT_RECORD_BYTES) return AGFT_E_WORKSPACE;
+    const size_t rec_bytes = (size_t)cfg->n_traces * chunk_steps * AGFT_RECORD_BYTES;
+    const size_t raw_bytes = cfg->closed.enable ? (size_t)cfg->n_traces * chunk_steps * AGFT_ROW_WORDS * 4 : 0;
+    if (scratch_bytes < rec_bytes + raw_bytes) return AGFT_E_WORKSPACE;
+    uint32_t *d_raw = cfg->closed.enable ? reinterpret_cast<uint32_t *>(static_cast<char *>(d_scratch) + rec_bytes)
+                                         : nullptr;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (cudaMemcpyAsync(d_params_buf, h_params, sizeof(agft_tuner_params) * cfg->n_tuners, cudaMemcpyHostToDevice,
                         s) != cudaSuccess)
@@ -510,8 +536,10 @@ agft_status agft_run(const agft_config *cfg, const agft_tuner_params *h_params, 
     if (st != AGFT_OK) return st;
     for (uint32_t t0 = 0; t0 < n_steps && st == AGFT_OK; t0 += chunk_steps) {
         const uint32_t n = (n_steps - t0) < chunk_steps ? (n_steps - t0) : chunk_steps;
-        st = agft_trace_generate(h, t0, n, d_scratch, nullptr);
-        if (st == AGFT_OK) st = agft_replay(h, d_scratch, t0, n, nullptr, nullptr);
+        st = agft_trace_generate(h, t0, n, d_scratch, d_raw);
+        if (st == AGFT_OK)
+            st = d_raw ? agft_replay_raw(h, d_scratch, d_raw, t0, n, nullptr, nullptr)
+                       : agft_replay(h, d_scratch, t0, n, nullptr, nullptr);
     }
     if (st == AGFT_OK) st = agft_stats(h, d_stats_buf);
     if (st == AGFT_OK &&

@@ -174,6 +174,13 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
     const uint32_t M = a.median_window;
 
     const StepRec *rp = a.records + (size_t)prm.trace_id * a.rec_stride + a.rec_off;
+    const uint32_t *rawp = (MODE == 0 && a.cl_enable) ? a.raw + ((size_t)prm.trace_id * a.rec_stride + a.rec_off) * AGFT_ROW_WORDS
+                                                      : nullptr;
+    uint32_t clq = 0u, clqb = 0u;                     // ENV-C backlogs (ENV.md §6)
+    if (rawp) {
+        clq = a.w.clq[tb * 2];
+        clqb = a.w.clq[tb * 2 + 1];
+    }
     double *bglob = a.w.b + tb * D * kMaxArms;
 
     for (uint32_t s = 0; s < a.n_steps; ++s) {
@@ -188,6 +195,40 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
             g = rec.g; invIm = rec.invIm; invAm = rec.invAm; wIm = rec.wIm;
             nT = rec.nT; nE = rec.nE; baseE = rec.baseE; baseEDP = rec.baseEDP;
             recI = rec.I; recP = rec.P;
+            if (rawp) {                               // ENV-C: both servers see their backlog (§6)
+                const uint32_t *rw = rawp + (size_t)s * AGFT_ROW_WORDS;
+                const uint32_t wr = rw[0], run = rw[1];
+                const uint32_t wq = wr + clq, wb = wr + clqb;
+                {                                     // x1 = queue presence (§4.1) of the tuner's server
+                    const double lo = a.norm_lo[0], hi = a.norm_hi[0];
+                    double xv = 0.0;
+                    if (hi > lo) {
+                        xv = xdiv(xsub(wq > 0 ? 1.0 : 0.0, lo), xsub(hi, lo));
+                        xv = xv < 0.0 ? 0.0 : (xv > 1.0 ? 1.0 : xv);
+                    }
+                    x[0] = xv;
+                }
+                const double rho = xdiv((double)(run + wq), (double)a.cap);
+                g = rho > 1.0 ? xmul(rho, xsqrt(rho)) : 1.0;
+                wIm = xmul((double)wq, invIm);
+                // the f_max baseline server with its own backlog (§3.3 at f_max_hw)
+                const double rhob = xdiv((double)(run + wb), (double)a.cap);
+                const double gb = rhob > 1.0 ? xmul(rhob, xsqrt(rhob)) : 1.0;
+                const double bdec = ec->base_dec, bpre = ec->base_pre, bpw = ec->base_pw;
+                const double bt_dec = xmul((double)recI, bdec);
+                const double bt_pre = xmul((double)recP, bpre);
+                const double bu = xmul(xmul(xadd(bt_dec, bt_pre), gb), invW);
+                const double bq = bu <= a.u_max ? xdiv(1.0, xsub(1.0, bu)) : xmul(bu, q_over);
+                const double btpot = xmul(xmul(xmul(xadd(bdec, xmul(bt_pre, invIm)), gb), bq), nT);
+                double bue = bu > 1.0 ? 1.0 : bu;
+                bue = bue < a.u_floor ? a.u_floor : bue;
+                baseE = xmul(xmul(xadd(a.p_idle, xmul(bpw, bue)), a.W), nE);
+                baseEDP = xmul(baseE, btpot);
+                const uint32_t arr = rw[6] + rw[7];
+                const uint32_t Db = arr + clqb;
+                const uint32_t sb = bu > 1.0 ? (uint32_t)floor(xdiv((double)Db, bu)) : Db;
+                clqb = min(a.cl_q_max, Db - sb);
+            }
         } else if constexpr (MODE == 1) {             // live: §4.1 context of the tuner's own snapshot
             const uint4 *rw = reinterpret_cast<const uint4 *>(a.live_rows + tb * AGFT_ROW_WORDS);
             const uint4 r0 = rw[0], r1 = rw[1];
@@ -304,6 +345,12 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
         const double busy = xmul(xadd(t_dec, t_pre), g);
         const double u = xmul(busy, invW);
         const double q = u <= a.u_max ? xdiv(1.0, xsub(1.0, u)) : xmul(u, q_over);
+        if (rawp) {                                   // ENV-C: requests this window leaves queued (§6)
+            const uint32_t *rw = rawp + (size_t)s * AGFT_ROW_WORDS;
+            const uint32_t Dq = rw[6] + rw[7] + clq;
+            const uint32_t sq = u > 1.0 ? (uint32_t)floor(xdiv((double)Dq, u)) : Dq;
+            clq = min(a.cl_q_max, Dq - sq);
+        }
         tpot = xmul(xmul(xmul(xadd(dec, xmul(t_pre, invIm)), g), q), nT);
         double ue = u > 1.0 ? 1.0 : u;
         ue = ue < a.u_floor ? a.u_floor : ue;
@@ -604,6 +651,10 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
         }
         const uint32_t bits = __ballot_sync(kFull, (act >> j) & 1u);
         if (lane == 0) a.w.active[tb * 4 + j] = bits;
+    }
+    if (rawp && lane == 0) {
+        a.w.clq[tb * 2] = clq;
+        a.w.clq[tb * 2 + 1] = clqb;
     }
     a.w.wsorted[tb * kWindow + 2 * lane] = wlo;
     a.w.wsorted[tb * kWindow + 2 * lane + 1] = whi;

@@ -164,7 +164,10 @@ __global__ void init_tuner_kernel(const __grid_constant__ InitArgs a)
             a.w.active[tb * 4 + k] = bits;
             a.w.extm[tb * 4 + k] = 0u;
         }
-        if (k < 2) a.w.wmeta[tb * 2 + k] = 0;
+        if (k < 2) {
+            a.w.wmeta[tb * 2 + k] = 0;
+            a.w.clq[tb * 2 + k] = 0;                    // ENV-C: no backlog at t = 0 (ENV.md §6)
+        }
         if (k == 0) {
             agft_tuner_stats st = {};
             st.traj_hash = kFnvOffset;

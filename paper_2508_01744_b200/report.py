@@ -39,13 +39,17 @@ def windowed(tb, T: int, bucket: int = 1) -> dict:
     prev = tb.stats()
     out = {k: [] for k in SERIES}
     out["steps"], out["t0"] = [], []
-    rec = None
+    rec = raw = None
+    closed = bool(getattr(tb, "closed", False))
     while t < T:
         m = min(bucket, T - t)
         if rec is None or rec.shape[1] != m:
             rec = tb.new_records(m)
-        tb.generate(t, m, rec)
-        tb.replay(rec, t, m)
+        if closed:                                    # ENV-C needs the raw rows (ENV.md §6)
+            rec, raw = tb.generate(t, m, rec, raw=True)
+        else:
+            tb.generate(t, m, rec)
+        tb.replay(rec, t, m, raw=raw) if closed else tb.replay(rec, t, m)
         cur = tb.stats()
         for k in SERIES:
             out[k].append(cur[_CUM[k]] - prev[_CUM[k]])
@@ -150,10 +154,13 @@ def main(argv=None):
     ap.add_argument("--bucket", type=int, default=1, help="windows per stats snapshot (1 = per-window CVs)")
     ap.add_argument("--split", type=int, default=231, help="convergence round when the phase switch is off")
     ap.add_argument("--phase", action="store_true", help="enable the Page-Hinkley switch (split = first_exploit_t)")
+    ap.add_argument("--closed", action="store_true", help="ENV-C closed-loop environment (ENV.md §6)")
     args = ap.parse_args(argv)
     cfg = dict(named_config(args.config), n_tuners=args.tuners, n_traces=args.tuners, sweep="none")
     if args.phase:
         cfg["ph_enable"] = 1
+    if args.closed:
+        cfg["cl_enable"] = 1
     params = tuner_params(cfg)
     ab = run_ablation(cfg, params, args.T, args.bucket)
     full = ab["series"]["full"]

@@ -365,14 +365,15 @@ static agft_status run_steps(agft_handle h, const void *d_records, uint32_t t0, 
         a.chosen = chosen;
         a.raw = raw;
         cudaError_t e = cudaSuccess;
-        // refinement re-admits arms, so a tuner's class can grow: one warp per tuner throughout;
-        // the closed loop (ENV.md §6) is implemented on the WIDE mapping only
-        if (c.kernel_policy == AGFT_POLICY_WIDE || c.refine.enable || c.closed.enable) {
+        // refinement re-admits arms, so a tuner's class can grow: one warp per tuner throughout
+        if (c.kernel_policy == AGFT_POLICY_WIDE || c.refine.enable) {
             e = launch_replay(a, c.d, h->stream);
         } else {
-            // MSEG and LANE do not implement the exploitation phase (ENV.md §4.10): AUTO instead
-            const bool split = c.kernel_policy != AGFT_POLICY_MSEG || c.phase.enable;
-            const bool lane = c.kernel_policy == AGFT_POLICY_LANE && lane_supported(c.d) && !c.phase.enable;
+            // MSEG and LANE implement neither the exploitation phase (ENV.md §4.10) nor the closed
+            // loop (§6): AUTO (SOLO / SEG2 / WIDE) instead
+            const bool ext = c.phase.enable || c.closed.enable;
+            const bool split = c.kernel_policy != AGFT_POLICY_MSEG || ext;
+            const bool lane = c.kernel_policy == AGFT_POLICY_LANE && lane_supported(c.d) && !ext;
             a.force_exact = lane_force_exact();
             e = launch_classify(h->ws, c.n_tuners, split, h->stream);
             if (e == cudaSuccess) e = cudaEventRecord(h->fork, h->stream);

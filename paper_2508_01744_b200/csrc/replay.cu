@@ -187,7 +187,7 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
         const uint32_t t = a.t0 + s;
         double x[D];
         double g = 0.0, invIm = 0.0, invAm = 0.0, wIm = 0.0, nT = 0.0, nE = 0.0, baseE = 0.0, baseEDP = 0.0;
-        uint32_t recI = 0u, recP = 0u;
+        uint32_t recI = 0u, recP = 0u, arr_cl = 0u;
         if constexpr (MODE == 0) {
             const StepRec &rec = rp[s];
 #pragma unroll
@@ -196,38 +196,14 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
             nT = rec.nT; nE = rec.nE; baseE = rec.baseE; baseEDP = rec.baseEDP;
             recI = rec.I; recP = rec.P;
             if (rawp) {                               // ENV-C: both servers see their backlog (§6)
-                const uint32_t *rw = rawp + (size_t)s * AGFT_ROW_WORDS;
-                const uint32_t wr = rw[0], run = rw[1];
-                const uint32_t wq = wr + clq, wb = wr + clqb;
-                {                                     // x1 = queue presence (§4.1) of the tuner's server
-                    const double lo = a.norm_lo[0], hi = a.norm_hi[0];
-                    double xv = 0.0;
-                    if (hi > lo) {
-                        xv = xdiv(xsub(wq > 0 ? 1.0 : 0.0, lo), xsub(hi, lo));
-                        xv = xv < 0.0 ? 0.0 : (xv > 1.0 ? 1.0 : xv);
-                    }
-                    x[0] = xv;
-                }
-                const double rho = xdiv((double)(run + wq), (double)a.cap);
-                g = rho > 1.0 ? xmul(rho, xsqrt(rho)) : 1.0;
-                wIm = xmul((double)wq, invIm);
-                // the f_max baseline server with its own backlog (§3.3 at f_max_hw)
-                const double rhob = xdiv((double)(run + wb), (double)a.cap);
-                const double gb = rhob > 1.0 ? xmul(rhob, xsqrt(rhob)) : 1.0;
-                const double bdec = ec->base_dec, bpre = ec->base_pre, bpw = ec->base_pw;
-                const double bt_dec = xmul((double)recI, bdec);
-                const double bt_pre = xmul((double)recP, bpre);
-                const double bu = xmul(xmul(xadd(bt_dec, bt_pre), gb), invW);
-                const double bq = bu <= a.u_max ? xdiv(1.0, xsub(1.0, bu)) : xmul(bu, q_over);
-                const double btpot = xmul(xmul(xmul(xadd(bdec, xmul(bt_pre, invIm)), gb), bq), nT);
-                double bue = bu > 1.0 ? 1.0 : bu;
-                bue = bue < a.u_floor ? a.u_floor : bue;
-                baseE = xmul(xmul(xadd(a.p_idle, xmul(bpw, bue)), a.W), nE);
-                baseEDP = xmul(baseE, btpot);
-                const uint32_t arr = rw[6] + rw[7];
-                const uint32_t Db = arr + clqb;
-                const uint32_t sb = bu > 1.0 ? (uint32_t)floor(xdiv((double)Db, bu)) : Db;
-                clqb = min(a.cl_q_max, Db - sb);
+                const ClosedRec cr = closed_record(rawp + (size_t)s * AGFT_ROW_WORDS, clq, clqb, recI, recP, invIm,
+                                                   nT, nE, ec, a);
+                x[0] = cr.x0;
+                g = cr.g;
+                wIm = cr.wIm;
+                baseE = cr.baseE;
+                baseEDP = cr.baseEDP;
+                arr_cl = cr.arr;
             }
         } else if constexpr (MODE == 1) {             // live: §4.1 context of the tuner's own snapshot
             const uint4 *rw = reinterpret_cast<const uint4 *>(a.live_rows + tb * AGFT_ROW_WORDS);
@@ -345,12 +321,7 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
         const double busy = xmul(xadd(t_dec, t_pre), g);
         const double u = xmul(busy, invW);
         const double q = u <= a.u_max ? xdiv(1.0, xsub(1.0, u)) : xmul(u, q_over);
-        if (rawp) {                                   // ENV-C: requests this window leaves queued (§6)
-            const uint32_t *rw = rawp + (size_t)s * AGFT_ROW_WORDS;
-            const uint32_t Dq = rw[6] + rw[7] + clq;
-            const uint32_t sq = u > 1.0 ? (uint32_t)floor(xdiv((double)Dq, u)) : Dq;
-            clq = min(a.cl_q_max, Dq - sq);
-        }
+        if (rawp) clq = closed_carry(arr_cl + clq, u, a.cl_q_max);   // ENV-C: left queued (§6)
         tpot = xmul(xmul(xmul(xadd(dec, xmul(t_pre, invIm)), g), q), nT);
         double ue = u > 1.0 ? 1.0 : u;
         ue = ue < a.u_floor ? a.u_floor : ue;

@@ -229,6 +229,13 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
     const StepRec *rp = a.records + (size_t)prm.trace_id * a.rec_stride + a.rec_off;
     const bool rec_on = prm.record_slot != AGFT_NO_RECORD;
     const double inv_tau = 1.0 / a.tau;
+    const uint32_t *rawp = a.cl_enable ? a.raw + ((size_t)prm.trace_id * a.rec_stride + a.rec_off) * AGFT_ROW_WORDS
+                                       : nullptr;
+    uint32_t clq = 0u, clqb = 0u;                                     // ENV-C backlogs (ENV.md §6)
+    if (rawp) {
+        clq = a.w.clq[(size_t)tb * 2];
+        clqb = a.w.clq[(size_t)tb * 2 + 1];
+    }
     __syncwarp();
 
     for (uint32_t s = 0; s < a.n_steps; ++s) {
@@ -237,6 +244,19 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
         double x[D];
 #pragma unroll
         for (int i = 0; i < D; ++i) x[i] = __ldg(&rc->x[i]);
+        double g = __ldg(&rc->g), wIm = __ldg(&rc->wIm), baseE = __ldg(&rc->baseE), baseEDP = __ldg(&rc->baseEDP);
+        uint32_t arr_cl = 0u;
+        if (rawp) {                                                   // ENV-C: the servers see their backlog
+            const ClosedRec cr = closed_record(rawp + (size_t)s * AGFT_ROW_WORDS, clq, clqb, __ldg(&rc->I),
+                                               __ldg(&rc->P), __ldg(&rc->invIm), __ldg(&rc->nT), __ldg(&rc->nE),
+                                               ec, a);
+            x[0] = cr.x0;
+            g = cr.g;
+            wIm = cr.wIm;
+            baseE = cr.baseE;
+            baseEDP = cr.baseEDP;
+            arr_cl = cr.arr;
+        }
         const double alpha = phase ? 0.0 : alpha_t(prm.alpha0, t, inv_tau);   // Exploitation: Eq. 2
 
         // ---- a4: both slots
@@ -298,9 +318,10 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
 
         // ---- a7: response
         const Response o = env_response(s_dec[kstar], s_pre[kstar], s_pw[kstar], __ldg(&rc->I), __ldg(&rc->P),
-                                        __ldg(&rc->g), __ldg(&rc->invIm), __ldg(&rc->invAm), __ldg(&rc->wIm),
+                                        g, __ldg(&rc->invIm), __ldg(&rc->invAm), wIm,
                                         __ldg(&rc->nT), __ldg(&rc->nE), invW, q_over, a.u_max, a.u_floor,
                                         a.p_idle, a.W);
+        if (rawp) clq = closed_carry(arr_cl + clq, o.u, a.cl_q_max);
         // ---- a8: reward + segment window
         double r = 0.0;
         if (wcount > 0) {
@@ -415,7 +436,7 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
 
         // ---- a11
         if (live && l == 0) {
-            stats_add(st, o, r, __ldg(&rc->baseE), __ldg(&rc->baseEDP), kstar, (uint32_t)nact0);
+            stats_add(st, o, r, baseE, baseEDP, kstar, (uint32_t)nact0);
             st.near_tie_steps += near ? 1u : 0u;
             if (rec_on) {
                 if (a.traj) a.traj[(size_t)prm.record_slot * a.rec_stride + a.rec_off + s] = (uint8_t)kstar;
@@ -460,6 +481,10 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
     }
     if (valid && l == 0) {
         *reinterpret_cast<uint4 *>(a.w.active + (size_t)tb * 4) = make_uint4(words[0], words[1], words[2], words[3]);
+        if (rawp) {
+            a.w.clq[(size_t)tb * 2] = clq;
+            a.w.clq[(size_t)tb * 2 + 1] = clqb;
+        }
         a.w.wmeta[(size_t)tb * 2] = wcount;
         a.w.wmeta[(size_t)tb * 2 + 1] = whead;
         st.n_active = (uint32_t)nact;

@@ -65,15 +65,37 @@ __global__ void __launch_bounds__(kSoloThreads, kSoloMinBlocks) solo_kernel(cons
     double *ring = a.w.wring + (size_t)tb * kWindow;
     const StepRec *rp = a.records + (size_t)prm.trace_id * a.rec_stride + a.rec_off;
     const bool rec_on = prm.record_slot != AGFT_NO_RECORD;
+    const uint32_t *rawp = a.cl_enable ? a.raw + ((size_t)prm.trace_id * a.rec_stride + a.rec_off) * AGFT_ROW_WORDS
+                                       : nullptr;
+    uint32_t clq = 0u, clqb = 0u;                                // ENV-C backlogs (ENV.md §6)
+    if (rawp) {
+        clq = a.w.clq[(size_t)tb * 2];
+        clqb = a.w.clq[(size_t)tb * 2 + 1];
+    }
 
     const SmemWindow win{S, kSoloThreads};
     double oldest = ring_oldest(ring, wcount, whead, M);
     for (uint32_t s = 0; s < a.n_steps; ++s) {
         const StepRec *rc = rp + s;                       // shared by the lanes of a trace: L1 broadcast
         // a7: response at the only active frequency
-        const Response o = env_response(dec, pre, pw, __ldg(&rc->I), __ldg(&rc->P), __ldg(&rc->g),
-                                        __ldg(&rc->invIm), __ldg(&rc->invAm), __ldg(&rc->wIm), __ldg(&rc->nT),
-                                        __ldg(&rc->nE), invW, q_over, a.u_max, a.u_floor, a.p_idle, a.W);
+        const uint32_t rI = __ldg(&rc->I), rP = __ldg(&rc->P);
+        const double rinvIm = __ldg(&rc->invIm), rnT = __ldg(&rc->nT), rnE = __ldg(&rc->nE);
+        double g = __ldg(&rc->g), wIm = __ldg(&rc->wIm), baseE = __ldg(&rc->baseE), baseEDP = __ldg(&rc->baseEDP);
+        double x0 = __ldg(&rc->x[0]);
+        uint32_t arr = 0u;
+        if (rawp) {                                              // ENV-C: the servers see their backlog
+            const ClosedRec cr = closed_record(rawp + (size_t)s * AGFT_ROW_WORDS, clq, clqb, rI, rP, rinvIm, rnT,
+                                               rnE, ec, a);
+            x0 = cr.x0;
+            g = cr.g;
+            wIm = cr.wIm;
+            baseE = cr.baseE;
+            baseEDP = cr.baseEDP;
+            arr = cr.arr;
+        }
+        const Response o = env_response(dec, pre, pw, rI, rP, g, rinvIm, __ldg(&rc->invAm), wIm, rnT, rnE, invW,
+                                        q_over, a.u_max, a.u_floor, a.p_idle, a.W);
+        if (rawp) clq = closed_carry(arr + clq, o.u, a.cl_q_max);
         // a8: reward against the median of the window, then push the EDP
         bool ok;
         const double r = reward_and_push(win, ring, wcount, whead, M, o.edp, a.clip_lo, a.clip_hi, ok, oldest);
@@ -89,10 +111,11 @@ __global__ void __launch_bounds__(kSoloThreads, kSoloMinBlocks) solo_kernel(cons
         double x[D];
 #pragma unroll
         for (int q = 0; q < D; ++q) x[q] = __ldg(&rc->x[q]);
+        x[0] = x0;
         sm_update<D>(A, th, b, x, r);
         welford(n, rbar, ebar, r, o.edp);
         // a11
-        stats_add(st, o, r, __ldg(&rc->baseE), __ldg(&rc->baseEDP), k, 1u);
+        stats_add(st, o, r, baseE, baseEDP, k, 1u);
         if (rec_on) {
             if (a.traj) a.traj[(size_t)prm.record_slot * a.rec_stride + a.rec_off + s] = (uint8_t)k;
             if (a.gap) a.gap[(size_t)prm.record_slot * a.rec_stride + a.rec_off + s] = kInf;
@@ -113,6 +136,10 @@ __global__ void __launch_bounds__(kSoloThreads, kSoloMinBlocks) solo_kernel(cons
     for (int j = 0; j < kWindow; ++j) a.w.wsorted[(size_t)tb * kWindow + j] = SW(j);
     a.w.wmeta[(size_t)tb * 2] = wcount;
     a.w.wmeta[(size_t)tb * 2 + 1] = whead;
+    if (rawp) {
+        a.w.clq[(size_t)tb * 2] = clq;
+        a.w.clq[(size_t)tb * 2 + 1] = clqb;
+    }
     st.n_active = 1;
     if (a.ph_enable) {
         a.w.ph[tb] = ph;

@@ -10,7 +10,7 @@ constexpr double kInf = __builtin_huge_val();
 
 // ENV.md §3.3: response at the chosen frequency (per-arm constants dec/pre/pw).
 struct Response {
-    double E, tpot, ttft, edp;
+    double E, tpot, ttft, edp, u;   // u: the window's utilisation busy/W (ENV-C backlog, ENV.md §6)
 };
 
 __device__ __forceinline__ Response env_response(double dec, double pre, double pw, uint32_t I, uint32_t P,
@@ -30,7 +30,64 @@ __device__ __forceinline__ Response env_response(double dec, double pre, double 
     o.E = xmul(xmul(xadd(p_idle, xmul(pw, ue)), W), nE);
     o.ttft = xmul(xadd(xmul(t_pre, invAm), xmul(t_dec, wIm)), q);
     o.edp = xmul(o.E, o.tpot);
+    o.u = u;
     return o;
+}
+
+// ---- ENV-C closed loop (ENV.md §6): the window as the tuner's server (carried backlog q) and
+// the f_max baseline server (backlog qb) see it.  Returns x1 (normalised), g and wIm of the
+// tuner's server and the baseline's (E, EDP); advances qb.  Exact arithmetic (ENV.md §0).
+struct ClosedRec {
+    double x0, g, wIm, baseE, baseEDP;
+    uint32_t arr;
+};
+
+__device__ __forceinline__ uint32_t closed_carry(uint32_t D, double u, uint32_t q_max)
+{
+    const uint32_t served = u > 1.0 ? (uint32_t)floor(xdiv((double)D, u)) : D;
+    return min(q_max, D - served);
+}
+
+__device__ __forceinline__ double rho_penalty(uint32_t running, uint32_t waiting, uint32_t cap)
+{
+    const double rho = xdiv((double)(running + waiting), (double)cap);
+    return rho > 1.0 ? xmul(rho, xsqrt(rho)) : 1.0;
+}
+
+__device__ __forceinline__ ClosedRec closed_record(const uint32_t *__restrict__ rw, uint32_t q, uint32_t &qb,
+                                                   uint32_t I, uint32_t P, double invIm, double nT, double nE,
+                                                   const EnvConsts *ec, const ReplayArgs &a)
+{
+    ClosedRec c;
+    const uint4 r0 = __ldg(reinterpret_cast<const uint4 *>(rw));
+    const uint4 r1 = __ldg(reinterpret_cast<const uint4 *>(rw) + 1);
+    const uint32_t wr = r0.x, run = r0.y;
+    c.arr = r1.z + r1.w;
+    const uint32_t wq = wr + q, wb = wr + qb;
+    {
+        const double lo = a.norm_lo[0], hi = a.norm_hi[0];
+        double xv = 0.0;
+        if (hi > lo) {
+            xv = xdiv(xsub(wq > 0 ? 1.0 : 0.0, lo), xsub(hi, lo));
+            xv = xv < 0.0 ? 0.0 : (xv > 1.0 ? 1.0 : xv);
+        }
+        c.x0 = xv;
+    }
+    c.g = rho_penalty(run, wq, a.cap);
+    c.wIm = xmul((double)wq, invIm);
+    const double gb = rho_penalty(run, wb, a.cap);
+    const double bdec = ec->base_dec, bpre = ec->base_pre, bpw = ec->base_pw;
+    const double bt_dec = xmul((double)I, bdec);
+    const double bt_pre = xmul((double)P, bpre);
+    const double bu = xmul(xmul(xadd(bt_dec, bt_pre), gb), ec->invW);
+    const double bq = bu <= a.u_max ? xdiv(1.0, xsub(1.0, bu)) : xmul(bu, ec->q_over);
+    const double btpot = xmul(xmul(xmul(xadd(bdec, xmul(bt_pre, invIm)), gb), bq), nT);
+    double bue = bu > 1.0 ? 1.0 : bu;
+    bue = bue < a.u_floor ? a.u_floor : bue;
+    c.baseE = xmul(xmul(xadd(a.p_idle, xmul(bpw, bue)), a.W), nE);
+    c.baseEDP = xmul(c.baseE, btpot);
+    qb = closed_carry(c.arr + qb, bu, a.cl_q_max);
+    return c;
 }
 
 // a8: r = clip(1 − EDP/ref) (AMB-3)

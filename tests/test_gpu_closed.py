@@ -28,13 +28,26 @@ def _device():
     (dict(pattern_mode=1, ph_enable=1, rf_enable=1), 2500, 1000),  # + phase switch + refinement
     (dict(pattern_mode=2, n_arms=1, prune_enable=0), 1500, 512),   # one low clock: a saturated queue
 ])
-def test_closed_loop_parity(kw, T, chunk):
+@pytest.mark.parametrize("policy", [0, 1])      # AUTO (SOLO / SEG2 / WIDE classes) and WIDE only
+def test_closed_loop_parity(kw, T, chunk, policy):
     cfg = with_overrides(named_config("C2"), cl_enable=1, n_tuners=6, n_traces=6, **kw)
     ids = list(range(6))
     params = tuner_params(cfg, ids)
     params["alpha0"] = np.array([0.0, 0.2, 0.5, 1.0, 2.0, 4.0])
-    tb, params, st, traj, _ = _run(cfg, T, params=params, record=ids, chunk=chunk)
+    tb, params, st, traj, _ = _run(cfg, T, params=params, record=ids, chunk=chunk, policy=policy)
     _check(cfg, tb, params, st, ids, T, traj)
+    tb.close()
+
+
+def test_closed_loop_c4_sampled():
+    """One C4 trace's 256 hyper-parameter points under ENV-C for 9,000 windows in the bench's
+    launch configuration (all classes, SOLO included); a sample checked against the oracle."""
+    cfg = with_overrides(named_config("C4"), cl_enable=1, n_traces=1)
+    ids = list(range(256))
+    params = tuner_params(cfg, ids)
+    sample = [0, 15, 48, 63, 100, 200, 255]
+    tb, params, st, traj, _ = _run(cfg, 9000, params=params, record=sample, chunk=4500)
+    _check(cfg, tb, params, st, sample, 9000, traj, slots={i: s for s, i in enumerate(sample)})
     tb.close()
 
 

@@ -100,10 +100,12 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
     extern __shared__ double smem[];
     double *s_dec = smem, *s_pre = smem + kMaxArms, *s_pw = smem + 2 * kMaxArms;
     const EnvConsts *ec = a.w.env;
-    for (int i = threadIdx.x; i < kMaxArms; i += blockDim.x) {
-        s_dec[i] = ec->dec[i];
-        s_pre[i] = ec->pre[i];
-        s_pw[i] = ec->pw[i];
+    if (MODE == 0) {                                  // the live modes take no dynamic shared memory
+        for (int i = threadIdx.x; i < kMaxArms; i += blockDim.x) {
+            s_dec[i] = ec->dec[i];
+            s_pre[i] = ec->pre[i];
+            s_pw[i] = ec->pw[i];
+        }
     }
     __syncthreads();
     const double invW = ec->invW, q_over = ec->q_over;
@@ -132,8 +134,14 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
         phase = s_ph[warp].phase;
     }
 
-    double *sA = smem + 3 * kMaxArms + (size_t)warp * S * (P + D) * 32;
-    double *sT = sA + S * P * 32;
+    // Arm state: the replay stages A⁻¹ and θ in shared memory for the whole launch
+    // ([slot][entry][lane]); a live window (MODE 1 / 2) reads and updates them in place in HBM
+    // (arm index fastest: 32 consecutive arms = one coalesced 256-B row), with no dynamic shared
+    // memory, so more tuners are in flight per SM.  Entry e of slot j: A[j * aJ + e * aS].
+    constexpr bool kInPlace = MODE != 0;
+    constexpr int aS = kInPlace ? kMaxArms : 32, aJ = kInPlace ? 32 : P * 32, tJ = kInPlace ? 32 : D * 32;
+    double *sA = kInPlace ? a.w.ainv + (size_t)tb * P * kMaxArms : smem + 3 * kMaxArms + (size_t)warp * S * (P + D) * 32;
+    double *sT = kInPlace ? a.w.theta + (size_t)tb * D * kMaxArms : sA + S * P * 32;
     const agft_tuner_params prm = a.w.params[tb];
     const uint32_t K = a.K;
 
@@ -150,8 +158,7 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
         const uint32_t k = 32u * j + lane;
         const bool on = k < K && ((a.w.active[tb * 4 + j] >> lane) & 1u);
         if (on) act |= 1u << j;
-        const bool ld = MODE == 0 || (MODE == 1 && on) || (MODE == 2 && (a.rf_enable || k == kpend));
-        if (ld) {
+        if (MODE == 0) {
 #pragma unroll
             for (int e = 0; e < P; ++e) sA[(j * P + e) * 32 + lane] = a.w.ainv[(tb * P + e) * kMaxArms + k];
 #pragma unroll
@@ -252,12 +259,12 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
             mg[j] = 0.0;
             if (__ballot_sync(kFull, (act >> j) & 1u) == 0) continue;
             if ((act >> j) & 1u) {
-                const double *Aj = sA + j * P * 32 + lane;
-                const double *Tj = sT + j * D * 32 + lane;
-                const double q = quad_form<P>(w, Aj, 32);
+                const double *Aj = sA + j * aJ + lane;
+                const double *Tj = sT + j * tJ + lane;
+                const double q = quad_form<P>(w, Aj, aS);
                 double p = 0.0;
 #pragma unroll
-                for (int i = 0; i < D; ++i) p = fma(Tj[i * 32], x[i], p);
+                for (int i = 0; i < D; ++i) p = fma(Tj[i * aS], x[i], p);
                 const double bonus = alpha * sqrt(fmax(q, 0.0));   // AMB-19
                 sc[j] = p + bonus;
                 mg[j] = fabs(p) + bonus;
@@ -372,11 +379,11 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
 
         // ---- a9: rank-1 update of the chosen arm (Eqs. 3–5) by its owner lane
         if (lane == own) {
-            double *Aj = sA + jst * P * 32 + lane;
-            double *Tj = sT + jst * D * 32 + lane;
+            double *Aj = sA + jst * aJ + lane;
+            double *Tj = sT + jst * tJ + lane;
             double Ap[P];
 #pragma unroll
-            for (int e = 0; e < P; ++e) Ap[e] = Aj[e * 32];
+            for (int e = 0; e < P; ++e) Ap[e] = Aj[e * aS];
             double z[D];
 #pragma unroll
             for (int i = 0; i < D; ++i) {
@@ -393,7 +400,7 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
 #pragma unroll
             for (int i = 0; i < D; ++i) {
                 xz = fma(x[i], z[i], xz);
-                th[i] = Tj[i * 32];
+                th[i] = Tj[i * aS];
                 px = fma(th[i], x[i], px);
             }
             const double invd = 1.0 / (1.0 + xz);              // Sherman–Morrison denominator
@@ -402,12 +409,12 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
 #pragma unroll
                 for (int r0 = 0; r0 < D; ++r0)
 #pragma unroll
-                    for (int c = r0; c < D; ++c, ++e) Aj[e * 32] = fma(-z[r0] * invd, z[c], Ap[e]);
+                    for (int c = r0; c < D; ++c, ++e) Aj[e * aS] = fma(-z[r0] * invd, z[c], Ap[e]);
             }
             const double coef = (r - px) * invd;                // RLS form of θ = A⁻¹ b (AMB-21)
 #pragma unroll
             for (int i = 0; i < D; ++i) {
-                Tj[i * 32] = fma(z[i], coef, th[i]);
+                Tj[i * aS] = fma(z[i], coef, th[i]);
                 double *bp = bglob + (size_t)i * kMaxArms + kstar;
                 *bp = xadd(*bp, xmul(r, x[i]));                // b exact, as Eq. 4 writes it
             }
@@ -543,12 +550,12 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
 #pragma unroll
                 for (int j = 0; j < S; ++j) {
                     if ((act >> j) & 1u) {
-                        const double *Aj = sA + j * P * 32 + lane;
-                        const double *Tj = sT + j * D * 32 + lane;
-                        const double q = quad_form<P>(wv, Aj, 32);
+                        const double *Aj = sA + j * aJ + lane;
+                        const double *Tj = sT + j * tJ + lane;
+                        const double q = quad_form<P>(wv, Aj, aS);
                         double p = 0.0;
 #pragma unroll
-                        for (int i = 0; i < D; ++i) p = fma(Tj[i * 32], x[i], p);
+                        for (int i = 0; i < D; ++i) p = fma(Tj[i * aS], x[i], p);
                         const double u = p + au * sqrt(fmax(q, 0.0));
                         if (u > bu) { bu = u; bk2 = 32 * j + lane; }
                     }
@@ -611,11 +618,13 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
 #pragma unroll
     for (int j = 0; j < S; ++j) {
         const uint32_t k = 32u * j + lane;
-        if (MODE == 0 || k == kpend) {                // a live window changed only the chosen arm
+        if (MODE == 0) {
 #pragma unroll
             for (int e = 0; e < P; ++e) a.w.ainv[(tb * P + e) * kMaxArms + k] = sA[(j * P + e) * 32 + lane];
 #pragma unroll
             for (int i = 0; i < D; ++i) a.w.theta[(tb * D + i) * kMaxArms + k] = sT[(j * D + i) * 32 + lane];
+        }
+        if (MODE == 0 || k == kpend) {                // a live window changed only the chosen arm's counters
             a.w.n[tb * kMaxArms + k] = n[j];
             a.w.rbar[tb * kMaxArms + k] = rbar[j];
             a.w.ebar[tb * kMaxArms + k] = ebar[j];
@@ -657,7 +666,7 @@ template <int D, int S, int MODE>
 static cudaError_t launch_ds(const ReplayArgs &a, cudaStream_t s)
 {
     constexpr int P = D * (D + 1) / 2;
-    const size_t smem = (3 * kMaxArms + (size_t)kWarpsPerBlock * S * (P + D) * 32) * sizeof(double);
+    const size_t smem = MODE == 0 ? (3 * kMaxArms + (size_t)kWarpsPerBlock * S * (P + D) * 32) * sizeof(double) : 0;
     auto kern = replay_kernel<D, S, MODE>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

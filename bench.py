@@ -50,6 +50,33 @@ def profile_traffic():
         return None, None
 
 
+def profile_utilisation():
+    """The three ncu utilisations SURVEY §8(d) asks for, of the dominant replay kernel, from the
+    committed ncu --set full capture (profiles/r01_v8_ncu_full_seg8.txt), or None."""
+    path = os.path.join(ROOT, "profiles", "r01_v8_ncu_full_seg8.txt")
+    keys = {"sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active": "fp64_pipe_pct",
+            "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed": "smem_pct",
+            "smsp__issue_active.avg.pct_of_peak_sustained_active": "issue_active_pct",
+            "sm__warps_active.avg.pct_of_peak_sustained_active": "warps_active_pct"}
+    out = {}
+    try:
+        with open(path) as f:
+            lines = f.read().splitlines()
+    except OSError:
+        return None
+    for ln in lines:
+        parts = ln.split()
+        if len(parts) >= 2 and parts[0] in keys:
+            out[keys[parts[0]]] = float(parts[1])
+        if ln.startswith("== "):
+            out["kernel"] = ln[3:].strip()
+        if parts and parts[0] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            out.setdefault("dram_mbytes", 0.0)
+            out["dram_mbytes"] += float(parts[1])
+    out["source"] = "profiles/r01_v8_ncu_full_seg8.txt (one launch, ncu --set full)"
+    return out
+
+
 def flops_per_step(d: int, k_act_sum: float, steps: float) -> float:
     """Algorithmic FP64 flops: per active arm d²+3d+3 (Eq. 1 score) + 5
     (pruning bookkeeping); per step 3d²+8d+4 (Sherman–Morrison + RLS update) + 50
@@ -119,11 +146,29 @@ def run_cpu_baseline(cfg: dict, n_tuners: int, T: int) -> dict:
     params = tuner_params(cfg, list(range(n_tuners)))
     cores = os.cpu_count() or 1
     t = time.perf_counter()
-    oracle.run_batch(cfg, params, T, threads=cores)
+    ost = oracle.run_batch(cfg, params, T, threads=cores)
     dt = time.perf_counter() - t
     return {"value": n_tuners * T / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": f"C4 tuners 0..{n_tuners - 1} (trace 0, all 256 hyper-parameter points) × {T} steps, "
-                      f"free-running, {dt:.1f} s on {cores} threads"}
+                      f"free-running, {dt:.1f} s on {cores} threads"}, ost
+
+
+PARITY_EXACT = ("steps", "n_active", "sum_active", "n_pruned_extreme", "n_pruned_hist", "n_pruned_cascade",
+                "sum_energy", "sum_tpot", "sum_ttft", "sum_edp", "sum_reward", "base_energy", "base_edp")
+
+
+def parity_summary(gst, ost) -> dict:
+    """The timed run's own statistics for the tuners the cpu_baseline leg ran through the oracle
+    (same config, same windows): trajectory-hash matches and, for those, exact equality of every
+    counter and fp64 sum (ENV.md §0).  A free-running oracle may leave the GPU's path at a near-tie
+    (ENV.md §4.5); the GPU's near-tie count is reported beside it."""
+    n = len(ost)
+    match = [i for i in range(n) if int(gst["traj_hash"][i]) == ost[i]["traj_hash"]]
+    exact = [i for i in match if all(gst[f][i] == ost[i][f] for f in PARITY_EXACT)]
+    return {"tuners": n, "traj_hash_match": len(match), "stats_exact_given_traj": len(exact),
+            "near_tie_steps_gpu": int(gst["near_tie_steps"][:n].astype(np.int64).sum()),
+            "fields": list(PARITY_EXACT),
+            "oracle": "free-running fp64 C oracle of the cpu_baseline leg, same config and windows"}
 
 
 def main():
@@ -279,7 +324,8 @@ def main():
                 "algorithmic_hbm_bytes_per_step": 128 * T * R + STATS_DTYPE.itemsize * n,   # records once + stats
                 "kernel": "replay_kernel", "replay_share": round(replay_ms / ms, 4),
                 "peak_source": "derived: 148 SM × 64 FP64 FMA/clk × 2 × sm_max_mhz (DESIGN.md §5)",
-                "mean_active_arms": round(sum_active / (float(n) * T), 3)}
+                "mean_active_arms": round(sum_active / (float(n) * T), 3),
+                "ncu_top_kernel": profile_utilisation()}
 
     out = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
@@ -299,7 +345,8 @@ def main():
     if not args.no_e2e:
         out["e2e"] = e2e_leg(cfg, params, sh.trace_base, world, local, chunk, n, T, args)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = run_cpu_baseline(cfg, 256, T)
+        out["cpu_baseline"], ost = run_cpu_baseline(cfg, 256, T)
+        out["parity"] = parity_summary(st, ost)
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:

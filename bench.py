@@ -149,7 +149,7 @@ def run_cpu_baseline(cfg: dict, n_tuners: int, T: int) -> dict:
     ost = oracle.run_batch(cfg, params, T, threads=cores)
     dt = time.perf_counter() - t
     return {"value": n_tuners * T / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"C4 tuners 0..{n_tuners - 1} (trace 0, all 256 hyper-parameter points) × {T} steps, "
+            "sample": f"{cfg.get('name', 'C4')} tuners 0..{n_tuners - 1} (trace 0, all 256 hyper-parameter points) × {T} steps, "
                       f"free-running, {dt:.1f} s on {cores} threads"}, ost
 
 

@@ -47,14 +47,22 @@ __device__ __forceinline__ int sisum(int v)
 }
 
 // sorted window element idx (S[l*E + e] in lane l of the segment)
+// (a binary mux tree on the bits of idx % E: a select chain here was compiled into a dynamically
+// indexed local-memory copy of the window — STL ×E/2 + LDL on the reward's serial chain)
 template <int G, int E>
 __device__ __forceinline__ double wat(const double (&S)[E], uint32_t idx)
 {
-    double v = S[0];
+    const uint32_t j = idx % E;
+    double v[E];
 #pragma unroll
-    for (int e = 1; e < E; ++e)
-        if ((idx % E) == (uint32_t)e) v = S[e];
-    return __shfl_sync(kFull, v, idx / E, G);
+    for (int e = 0; e < E; ++e) v[e] = S[e];
+#pragma unroll
+    for (int b = 1; b < E; b <<= 1) {
+        const bool up = (j & (uint32_t)b) != 0u;
+#pragma unroll
+        for (int e = 0; e + b < E; e += 2 * b) v[e] = up ? v[e + b] : v[e];
+    }
+    return __shfl_sync(kFull, v[0], idx / E, G);
 }
 template <int G, int E>
 __device__ __forceinline__ int wless(const double (&S)[E], double v)

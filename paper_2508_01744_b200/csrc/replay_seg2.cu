@@ -128,11 +128,18 @@ __device__ __forceinline__ double stree(double *buf, int l, bool h0, int k0, dou
     return s;
 }
 
+// b of both slots is staged in shared memory next to A⁻¹ when it fits at 4 blocks per SM
+// (G ≥ 8): its read-modify-write in the Sherman–Morrison step is on the serial chain, and a
+// global-memory round trip there stalled the warp (ncu source attribution)
 template <int G>
-constexpr size_t seg2_smem_bytes(int P)
+__host__ __device__ constexpr bool b_in_smem() { return G >= 8; }
+
+template <int G>
+constexpr size_t seg2_smem_bytes(int P, int D)
 {
     return (3 * kMaxArms + (size_t)kSeg2Warps * 2 * P * 32 + (size_t)kSeg2Warps * (32 / G) * tree_stride<G>()) * 8 +
-           (size_t)kSeg2Warps * (32 / G) * sizeof(agft_tuner_stats);
+           (size_t)kSeg2Warps * (32 / G) * sizeof(agft_tuner_stats) +
+           (b_in_smem<G>() ? (size_t)kSeg2Warps * 2 * D * 32 * 8 : 0);
 }
 
 }  // namespace
@@ -148,6 +155,7 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
     double *s_A = sm + 3 * kMaxArms;                                   // [warp][slot][P][32]
     double *s_tree = s_A + kSeg2Warps * 2 * P * 32;                    // [warp][seg][tree_stride]
     agft_tuner_stats *s_st = reinterpret_cast<agft_tuner_stats *>(s_tree + kSeg2Warps * NSEG * tree_stride<G>());
+    double *s_B = reinterpret_cast<double *>(s_st + kSeg2Warps * NSEG);  // [warp][slot][D][32] (G ≥ 8)
     const EnvConsts *ec = a.w.env;
     for (int q = threadIdx.x; q < kMaxArms; q += blockDim.x) {
         s_dec[q] = ec->dec[q];
@@ -233,6 +241,15 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
     const uint32_t M = a.median_window;
     double *ring = a.w.wring + (size_t)tb * kWindow;
     double *bg = a.w.b + (size_t)tb * D * kMaxArms;
+    constexpr bool kBS = b_in_smem<G>();
+    double *B0 = s_B + (warp * 2 + 0) * D * 32 + lane, *B1 = s_B + (warp * 2 + 1) * D * 32 + lane;
+    if (kBS) {
+#pragma unroll
+        for (int r = 0; r < D; ++r) {
+            B0[r * 32] = has0 ? bg[(size_t)r * kMaxArms + key0] : 0.0;
+            B1[r * 32] = has1 ? bg[(size_t)r * kMaxArms + key1] : 0.0;
+        }
+    }
     int nact = spopc<G>(act0, sg) + spopc<G>(act1, sg);
     const StepRec *rp = a.records + (size_t)prm.trace_id * a.rec_stride + a.rec_off;
     const bool rec_on = prm.record_slot != AGFT_NO_RECORD;
@@ -371,7 +388,8 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
             double thv[D];
 #pragma unroll
             for (int i = 0; i < D; ++i) thv[i] = oslot ? th1[i] : th0[i];
-            sm_update_smem<D>(oslot ? A1 : A0, 32, thv, bg + kstar, kMaxArms, x, r);
+            if (kBS) sm_update_smem<D>(oslot ? A1 : A0, 32, thv, oslot ? B1 : B0, 32, x, r);
+            else sm_update_smem<D>(oslot ? A1 : A0, 32, thv, bg + kstar, kMaxArms, x, r);
 #pragma unroll
             for (int i = 0; i < D; ++i) {
                 if (oslot) th1[i] = thv[i]; else th0[i] = thv[i];
@@ -465,6 +483,10 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
             a.w.n[(size_t)tb * kMaxArms + key0] = n0;
             a.w.rbar[(size_t)tb * kMaxArms + key0] = rb0;
             a.w.ebar[(size_t)tb * kMaxArms + key0] = eb0;
+            if (kBS) {
+#pragma unroll
+                for (int r = 0; r < D; ++r) bg[(size_t)r * kMaxArms + key0] = B0[r * 32];
+            }
         }
         if (has1) {
 #pragma unroll
@@ -474,6 +496,10 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
             a.w.n[(size_t)tb * kMaxArms + key1] = n1;
             a.w.rbar[(size_t)tb * kMaxArms + key1] = rb1;
             a.w.ebar[(size_t)tb * kMaxArms + key1] = eb1;
+            if (kBS) {
+#pragma unroll
+                for (int r = 0; r < D; ++r) bg[(size_t)r * kMaxArms + key1] = B1[r * 32];
+            }
         }
 #pragma unroll
         for (int e = 0; e < E; ++e) a.w.wsorted[(size_t)tb * kWindow + l * E + e] = S[e];
@@ -509,7 +535,7 @@ static cudaError_t launch_seg2_dg(const ReplayArgs &a, cudaStream_t s)
 {
     constexpr int P = D * (D + 1) / 2;
     constexpr int per_block = kSeg2Warps * (32 / G);
-    const size_t smem = seg2_smem_bytes<G>(P);
+    const size_t smem = seg2_smem_bytes<G>(P, D);
     auto kern = seg2_kernel<D, G>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

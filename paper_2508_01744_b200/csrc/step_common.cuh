@@ -309,12 +309,16 @@ template <int D>
 __device__ __forceinline__ void sm_update_smem(double *Ac, int stride, double (&th)[D], double *bcol,
                                                int bstride, const double (&x)[D], double r)
 {
+    constexpr int P = D * (D + 1) / 2;
+    double Ap[P];                                   // each packed entry read once (not twice)
+#pragma unroll
+    for (int e = 0; e < P; ++e) Ap[e] = Ac[e * stride];
     double z[D];
 #pragma unroll
     for (int i = 0; i < D; ++i) {
         double acc = 0.0;
 #pragma unroll
-        for (int c = 0; c < D; ++c) acc = fma(Ac[(i <= c ? pidx<D>(i, c) : pidx<D>(c, i)) * stride], x[c], acc);
+        for (int c = 0; c < D; ++c) acc = fma(Ap[i <= c ? pidx<D>(i, c) : pidx<D>(c, i)], x[c], acc);
         z[i] = acc;
     }
     double xz = 0.0, px = 0.0;
@@ -328,10 +332,7 @@ __device__ __forceinline__ void sm_update_smem(double *Ac, int stride, double (&
     for (int r0 = 0; r0 < D; ++r0) {
         const double zr = -z[r0] * invd;
 #pragma unroll
-        for (int c = r0; c < D; ++c) {
-            double &ae = Ac[pidx<D>(r0, c) * stride];
-            ae = fma(zr, z[c], ae);
-        }
+        for (int c = r0; c < D; ++c) Ac[pidx<D>(r0, c) * stride] = fma(zr, z[c], Ap[pidx<D>(r0, c)]);
     }
     const double coef = (r - px) * invd;
 #pragma unroll

@@ -2,7 +2,7 @@
 # names are matched on the demangled base: "void agft::seg2_kernel<(int)7, (int)8>(agft::ReplayArgs)"
 TAG=${TAG:-r01}
 B="python bench.py --T ${PT:-16384} --steps 1 --warmup 0 --no-cpu-baseline --no-e2e"
-N="ncu --set full --clock-control none --import-source on"
+N="ncu --set full --clock-control none --import-source on --kernel-name-base demangled"
 mkdir -p gpurun_out
 for K in ${KERNELS:-seg2_kernel_7_8 solo_kernel_7}; do
   case $K in

@@ -240,6 +240,7 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
     uint32_t wcount = a.w.wmeta[(size_t)tb * 2], whead = a.w.wmeta[(size_t)tb * 2 + 1];
     const uint32_t M = a.median_window;
     double *ring = a.w.wring + (size_t)tb * kWindow;
+    double oldest = wcount == M ? ring[whead] : 0.0;                  // the value the next push evicts
     double *bg = a.w.b + (size_t)tb * D * kMaxArms;
     constexpr bool kBS = b_in_smem<G>();
     double *B0 = s_B + (warp * 2 + 0) * D * 32 + lane, *B1 = s_B + (warp * 2 + 1) * D * 32 + lane;
@@ -375,12 +376,21 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
             winsert<G, E>(S, o.edp, wless<G, E>(S, o.edp), l);
             if (live && l == 0) ring[wcount] = o.edp;
             ++wcount;
+            if (wcount == M) oldest = M == 1 ? o.edp : ring[whead];   // prefetch the next eviction
         } else {
-            const double old = ring[whead];
-            wremove<G, E>(S, wless<G, E>(S, old), l);
-            winsert<G, E>(S, o.edp, wless<G, E>(S, o.edp), l);
+            const double old = oldest;
+            // both ranks from ONE butterfly on the current window: #(S' < v) after removing `old`
+            // is #(S < v) − [old < v], exactly (multiset identity)
+            int c = 0;
+#pragma unroll
+            for (int e = 0; e < E; ++e) c += ((S[e] < old) ? 1 : 0) + ((S[e] < o.edp) ? 0x10000 : 0);
+            c = sisum<G>(c);
+            const int po = c & 0xffff, pv = (c >> 16) - ((old < o.edp) ? 1 : 0);
+            wremove<G, E>(S, po, l);
+            winsert<G, E>(S, o.edp, pv, l);
             if (live && l == 0) ring[whead] = o.edp;
             whead = (whead + 1 == M) ? 0u : whead + 1;
+            oldest = M == 1 ? o.edp : ring[whead];     // next step's eviction, loaded off the chain
         }
 
         // ---- a9: Sherman–Morrison on the owner lane's slot

@@ -267,6 +267,7 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
     for (uint32_t s = 0; s < a.n_steps; ++s) {
         const uint32_t t = a.t0 + s;
         const StepRec *rc = rp + s;
+        if (s + 1 < a.n_steps && l == 0) prefetch_l1(rc + 1);
         double x[D];
 #pragma unroll
         for (int i = 0; i < D; ++i) x[i] = __ldg(&rc->x[i]);

@@ -77,6 +77,7 @@ __global__ void __launch_bounds__(kSoloThreads, kSoloMinBlocks) solo_kernel(cons
     double oldest = ring_oldest(ring, wcount, whead, M);
     for (uint32_t s = 0; s < a.n_steps; ++s) {
         const StepRec *rc = rp + s;                       // shared by the lanes of a trace: L1 broadcast
+        if (s + 1 < a.n_steps) prefetch_l1(rc + 1);
         // a7: response at the only active frequency
         const uint32_t rI = __ldg(&rc->I), rP = __ldg(&rc->P);
         const double rinvIm = __ldg(&rc->invIm), rnT = __ldg(&rc->nT), rnE = __ldg(&rc->nE);

@@ -90,6 +90,10 @@ __device__ __forceinline__ ClosedRec closed_record(const uint32_t *__restrict__ 
     return c;
 }
 
+// L1 prefetch of the next window's 128-B step record: its fields head the next step's serial
+// chain (context → scores), so the L2 round trip is taken off it (no register cost)
+__device__ __forceinline__ void prefetch_l1(const void *p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+
 // a8: r = clip(1 − EDP/ref) (AMB-3)
 __device__ __forceinline__ double reward_of(double edp, double ref, double lo, double hi)
 {

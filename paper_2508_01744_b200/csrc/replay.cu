@@ -197,7 +197,10 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
         uint32_t recI = 0u, recP = 0u, arr_cl = 0u;
         if constexpr (MODE == 0) {
             const StepRec &rec = rp[s];
-            if (s + 1 < a.n_steps && lane == 0) prefetch_l1(&rp[s + 1]);
+            if (s + 1 < a.n_steps && lane == 0) {
+                prefetch_l1(&rp[s + 1]);
+                if (rawp) prefetch_l1(rawp + (size_t)(s + 1) * AGFT_ROW_WORDS);
+            }
 #pragma unroll
             for (int i = 0; i < D; ++i) x[i] = rec.x[i];
             g = rec.g; invIm = rec.invIm; invAm = rec.invAm; wIm = rec.wIm;

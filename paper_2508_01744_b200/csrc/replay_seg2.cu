@@ -267,7 +267,10 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
     for (uint32_t s = 0; s < a.n_steps; ++s) {
         const uint32_t t = a.t0 + s;
         const StepRec *rc = rp + s;
-        if (s + 1 < a.n_steps && l == 0) prefetch_l1(rc + 1);
+        if (s + 1 < a.n_steps && l == 0) {
+            prefetch_l1(rc + 1);
+            if (rawp) prefetch_l1(rawp + (size_t)(s + 1) * AGFT_ROW_WORDS);
+        }
         double x[D];
 #pragma unroll
         for (int i = 0; i < D; ++i) x[i] = __ldg(&rc->x[i]);
@@ -285,6 +288,17 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
             arr_cl = cr.arr;
         }
         const double alpha = phase ? 0.0 : alpha_t(prm.alpha0, t, inv_tau);   // Exploitation: Eq. 2
+        // the reward's reference (median of the window before this step's push) depends only on
+        // the window: computed here, off the response → reward chain
+        double ref = 0.0;
+        if (wcount > 0) {
+            if (wcount & 1u) {
+                ref = wat<G, E>(S, wcount >> 1);
+            } else {
+                const double m0 = wat<G, E>(S, (wcount >> 1) - 1), m1 = wat<G, E>(S, wcount >> 1);
+                ref = xmul(xadd(m0, m1), 0.5);
+            }
+        }
 
         // ---- a4: both slots
         double w[P];
@@ -325,6 +339,7 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
         const double mstar = __shfl_sync(kFull, oslot ? mg1 : mg0, own, G);
         const bool fstar = __shfl_sync(kFull, (int)((oslot ? n1 : n0) == 0u), own, G) != 0;
         const bool own0 = is_own && oslot == 0, own1 = is_own && oslot == 1;
+        const double inv_n = xdiv(1.0, (double)((oslot ? n1 : n0) + 1u));   // Welford's 1/n, off the chain
         const bool tie = (act0 && !own0 && (bs - sc0 < a.tie_rel * fmax(mstar, mg0)) && !(fstar && n0 == 0u)) ||
                          (act1 && !own1 && (bs - sc1 < a.tie_rel * fmax(mstar, mg1)) && !(fstar && n1 == 0u));
         const bool near = sbits<G>(tie, sg) != 0u;
@@ -352,13 +367,6 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
         // ---- a8: reward + segment window
         double r = 0.0;
         if (wcount > 0) {
-            double ref;
-            if (wcount & 1u) {
-                ref = wat<G, E>(S, wcount >> 1);
-            } else {
-                const double m0 = wat<G, E>(S, (wcount >> 1) - 1), m1 = wat<G, E>(S, wcount >> 1);
-                ref = xmul(xadd(m0, m1), 0.5);
-            }
             r = reward_of(o.edp, ref, a.clip_lo, a.clip_hi);
         }
         if (!isfinite(o.edp) || !isfinite(r)) {
@@ -405,8 +413,8 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
             for (int i = 0; i < D; ++i) {
                 if (oslot) th1[i] = thv[i]; else th0[i] = thv[i];
             }
-            if (oslot) welford(n1, rb1, eb1, r, o.edp);
-            else welford(n0, rb0, eb0, r, o.edp);
+            if (oslot) welford_inv(n1, rb1, eb1, r, o.edp, inv_n);
+            else welford_inv(n0, rb0, eb0, r, o.edp, inv_n);
         }
 
         // ---- a10: pruning (ENV.md §4.8)

@@ -77,7 +77,14 @@ __global__ void __launch_bounds__(kSoloThreads, kSoloMinBlocks) solo_kernel(cons
     double oldest = ring_oldest(ring, wcount, whead, M);
     for (uint32_t s = 0; s < a.n_steps; ++s) {
         const StepRec *rc = rp + s;                       // shared by the lanes of a trace: L1 broadcast
-        if (s + 1 < a.n_steps) prefetch_l1(rc + 1);
+        if (s + 1 < a.n_steps) {
+            prefetch_l1(rc + 1);
+            if (rawp) prefetch_l1(rawp + (size_t)(s + 1) * AGFT_ROW_WORDS);
+        }
+        // off the chain: the reward's reference (median of the window before this push) and
+        // Welford's 1/n depend only on the tuner's state at the start of the step
+        const double ref = wcount > 0 ? win.median(wcount) : 0.0;
+        const double inv_n = xdiv(1.0, (double)(n + 1u));
         // a7: response at the only active frequency
         const uint32_t rI = __ldg(&rc->I), rP = __ldg(&rc->P);
         const double rinvIm = __ldg(&rc->invIm), rnT = __ldg(&rc->nT), rnE = __ldg(&rc->nE);
@@ -98,12 +105,12 @@ __global__ void __launch_bounds__(kSoloThreads, kSoloMinBlocks) solo_kernel(cons
                                         q_over, a.u_max, a.u_floor, a.p_idle, a.W);
         if (rawp) clq = closed_carry(arr + clq, o.u, a.cl_q_max);
         // a8: reward against the median of the window, then push the EDP
-        bool ok;
-        const double r = reward_and_push(win, ring, wcount, whead, M, o.edp, a.clip_lo, a.clip_hi, ok, oldest);
-        if (!ok) {
+        const double r = wcount > 0 ? reward_of(o.edp, ref, a.clip_lo, a.clip_hi) : 0.0;
+        if (!isfinite(o.edp) || !isfinite(r)) {
             st.flags |= 1u;
             break;
         }
+        push_edp(win, ring, wcount, whead, M, o.edp, oldest);
         if (a.ph_enable) {                                       // ENV.md §4.10 (one arm: α is moot)
             ph.exploit_steps += ph.phase;
             ph_observe(ph, r, a.t0 + s, a.ph_window, a.ph_delta, a.ph_lambda);
@@ -114,7 +121,7 @@ __global__ void __launch_bounds__(kSoloThreads, kSoloMinBlocks) solo_kernel(cons
         for (int q = 0; q < D; ++q) x[q] = __ldg(&rc->x[q]);
         x[0] = x0;
         sm_update<D>(A, th, b, x, r);
-        welford(n, rbar, ebar, r, o.edp);
+        welford_inv(n, rbar, ebar, r, o.edp, inv_n);
         // a11
         stats_add(st, o, r, baseE, baseEDP, k, 1u);
         if (rec_on) {

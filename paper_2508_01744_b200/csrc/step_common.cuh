@@ -110,6 +110,14 @@ __device__ __forceinline__ void welford(uint32_t &n, double &rbar, double &ebar,
     ebar = xadd(ebar, xmul(xsub(edp, ebar), inv));
 }
 
+// the same with 1/(n+1) computed earlier, off the reward chain (identical values)
+__device__ __forceinline__ void welford_inv(uint32_t &n, double &rbar, double &ebar, double r, double edp, double inv)
+{
+    n += 1u;
+    rbar = xadd(rbar, xmul(xsub(r, rbar), inv));
+    ebar = xadd(ebar, xmul(xsub(edp, ebar), inv));
+}
+
 // ENV.md §4.10 observe_reward: the Page-Hinkley detector on the reward of step t (after a8)
 __device__ __forceinline__ void ph_observe(PhState &p, double r, uint32_t t, uint32_t W, double delta, double lambda)
 {
@@ -278,6 +286,9 @@ struct SmemWindow {
     }
 };
 
+__device__ __forceinline__ void push_edp(const SmemWindow &win, double *ring, uint32_t &wcount, uint32_t &whead,
+                                         uint32_t M, double edp, double &oldest);
+
 // a8 for a lane-private window: reward against the median of the window, then push edp.
 // `oldest` carries the ring value that the next push evicts (ring[whead] of a full window),
 // loaded one step ahead so its global-memory latency overlaps the step.
@@ -289,6 +300,14 @@ __device__ __forceinline__ double reward_and_push(const SmemWindow &win, double 
     if (wcount > 0) r = reward_of(edp, win.median(wcount), clip_lo, clip_hi);
     finite_ok = isfinite(edp) && isfinite(r);
     if (!finite_ok) return r;
+    push_edp(win, ring, wcount, whead, M, edp, oldest);
+    return r;
+}
+
+// push edp into a lane-private window (the second half of reward_and_push)
+__device__ __forceinline__ void push_edp(const SmemWindow &win, double *ring, uint32_t &wcount, uint32_t &whead,
+                                         uint32_t M, double edp, double &oldest)
+{
     if (wcount < M) {
         win.insert(wcount, edp);
         ring[wcount] = edp;
@@ -299,7 +318,6 @@ __device__ __forceinline__ double reward_and_push(const SmemWindow &win, double 
         whead = (whead + 1 == M) ? 0u : whead + 1;
     }
     if (wcount == M) oldest = ring[whead];
-    return r;
 }
 
 __device__ __forceinline__ double ring_oldest(const double *ring, uint32_t wcount, uint32_t whead, uint32_t M)

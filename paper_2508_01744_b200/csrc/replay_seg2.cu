@@ -102,8 +102,10 @@ __host__ __device__ constexpr int tree_stride() { return 128 + G + 1; }
 template <int G>
 __device__ __forceinline__ int tslot(int k) { return k + k / (128 / G); }
 
-// canonical tree: scatter (has0,key0,v0), (has1,key1,v1) of every lane to `buf` (zeros on
-// entry, restored to zeros on exit), reduce aligned blocks pairwise, butterfly
+// canonical tree: scatter (has0,key0,v0), (has1,key1,v1) of every lane to `buf`, reduce aligned
+// blocks pairwise, butterfly.  Slots outside the scattered set must hold +0.0: the caller scatters
+// the same set Q (active arms with n ≥ hist_n) in both trees of a step, Q only grows between steps
+// except by pruning, and a pruned arm's slot is zeroed when it is removed (no restore pass here)
 template <int G>
 __device__ __forceinline__ double stree(double *buf, int l, bool h0, int k0, double v0, bool h1, int k1, double v1)
 {
@@ -121,10 +123,7 @@ __device__ __forceinline__ double stree(double *buf, int l, bool h0, int k0, dou
     double s = v[0];
 #pragma unroll
     for (int off = 1; off < G; off <<= 1) s = xadd(s, __shfl_xor_sync(kFull, s, off, G));
-    __syncwarp();
-    if (h0) buf[tslot<G>(k0)] = 0.0;
-    if (h1) buf[tslot<G>(k1)] = 0.0;
-    __syncwarp();
+    __syncwarp();                                     // reads done before the next scatter / zeroing
     return s;
 }
 
@@ -474,8 +473,14 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
                     }
                     nact -= ce + ch + cc;
                 }
-                if (rm0) act0 = false;
-                if (rm1) act1 = false;
+                if (rm0) {
+                    act0 = false;
+                    tree[tslot<G>(key0)] = 0.0;       // keep the tree buffer's non-Q slots at +0.0
+                }
+                if (rm1) {
+                    act1 = false;
+                    tree[tslot<G>(key1)] = 0.0;
+                }
             }
         }
 

@@ -275,12 +275,29 @@ struct SmemWindow {
     {
         const int po = count_less((int)M, old);            // S[po] == old
         const int lv = count_less((int)M, v);               // #(S < v), old included
+        // the shifts move up to 63 entries and their lengths differ between the lanes of a warp:
+        // 8 entries per iteration (all 8 loads issued before the 8 stores) instead of one, so the
+        // divergent loop runs ≤ 8 times and its loads overlap
         if (v < old) {                                      // v lands at lv ≤ po: shift [lv, po) up
-            for (int j = po; j > lv; --j) at(j) = at(j - 1);
+            for (int j0 = po; j0 > lv; j0 -= 8) {
+                double t[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) t[k] = at(max(j0 - 1 - k, 0));
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    if (j0 - k > lv) at(j0 - k) = t[k];
+            }
             at(lv) = v;
         } else if (v > old) {                               // v lands at lv − 1 ≥ po: shift (po, lv) down
             const int pn = lv - 1;
-            for (int j = po; j < pn; ++j) at(j) = at(j + 1);
+            for (int j0 = po; j0 < pn; j0 += 8) {
+                double t[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) t[k] = at(min(j0 + 1 + k, kWindow - 1));
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    if (j0 + k < pn) at(j0 + k) = t[k];
+            }
             at(pn) = v;
         }                                                   // v == old: the multiset is unchanged
     }

@@ -269,12 +269,26 @@ struct SmemWindow {
         for (int j = (int)n; j > p; --j) at(j) = at(j - 1);
         at(p) = v;
     }
-    // replace `old` (present) by v in a full window of M values: both positions by binary
-    // search (independent), then shift the elements between them by one slot
+    // #(S[0..64) < v) in two dependent shared-memory round trips instead of seven: the 8 block
+    // maxima S[8i+7] say how many whole blocks are below v, then the 8 entries of the next block.
+    // Entries past the count are +inf, so this equals count_less(n, v) for any n ≤ 64 and finite v.
+    __device__ __forceinline__ int count_less64(double v) const
+    {
+        int c = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) c += at(8 * i + 7) < v ? 1 : 0;
+        if (c == 8) return 64;
+        int r = 8 * c;
+#pragma unroll
+        for (int k = 0; k < 7; ++k) r += at(8 * c + k) < v ? 1 : 0;
+        return r;
+    }
+    // replace `old` (present) by v in a full window of M values: both positions (independent),
+    // then shift the elements between them by one slot
     __device__ __forceinline__ void replace(uint32_t M, double old, double v) const
     {
-        const int po = count_less((int)M, old);            // S[po] == old
-        const int lv = count_less((int)M, v);               // #(S < v), old included
+        const int po = count_less64(old);                   // S[po] == old
+        const int lv = count_less64(v);                     // #(S < v), old included
         // the shifts move up to 63 entries and their lengths differ between the lanes of a warp:
         // 8 entries per iteration (all 8 loads issued before the 8 stores) instead of one, so the
         // divergent loop runs ≤ 8 times and its loads overlap

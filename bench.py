@@ -39,21 +39,21 @@ N_SM = 148
 
 def profile_traffic():
     """DRAM bytes (read + write) of all replay-class launches of one default bench step, from
-    the committed ncu capture (tools/gpu_traffic.sh → profiles/r01_v8_traffic.json), or None."""
-    path = os.path.join(ROOT, "profiles", "r01_v8_traffic.json")
+    the committed ncu capture (tools/gpu_traffic.sh → profiles/r01_v13_traffic.json), or None."""
+    path = os.path.join(ROOT, "profiles", "r01_v13_traffic.json")
     try:
         with open(path) as f:
             tot = json.load(f)["_replay_total"]
         return tot["dram_bytes"], ("ncu dram__bytes_read+write summed over the replay launches of one "
-                                   "C4 bench step (profiles/r01_v8_traffic.json)")
+                                   "C4 bench step (profiles/r01_v13_traffic.json)")
     except (OSError, KeyError, ValueError):
         return None, None
 
 
 def profile_utilisation():
     """The three ncu utilisations SURVEY §8(d) asks for, of the dominant replay kernel, from the
-    committed ncu --set full capture (profiles/r01_v8_ncu_full_seg8.txt), or None."""
-    path = os.path.join(ROOT, "profiles", "r01_v8_ncu_full_seg8.txt")
+    committed ncu --set full capture (profiles/r01_v13_ncu_full_seg8.txt), or None."""
+    path = os.path.join(ROOT, "profiles", "r01_v13_ncu_full_seg8.txt")
     keys = {"sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active": "fp64_pipe_pct",
             "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed": "smem_pct",
             "smsp__issue_active.avg.pct_of_peak_sustained_active": "issue_active_pct",
@@ -73,7 +73,7 @@ def profile_utilisation():
         if parts and parts[0] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
             out.setdefault("dram_mbytes", 0.0)
             out["dram_mbytes"] += float(parts[1])
-    out["source"] = "profiles/r01_v8_ncu_full_seg8.txt (one launch, ncu --set full)"
+    out["source"] = "profiles/r01_v13_ncu_full_seg8.txt (one launch, ncu --set full)"
     return out
 
 

@@ -12,6 +12,7 @@ for K in ${KERNELS:-seg2_kernel_7_8 solo_kernel_7}; do
     seg2_kernel_7_32) RX='regex:seg2_kernel<\(int\)7, \(int\)32>' ;;
     solo_kernel_7) RX='regex:solo_kernel<\(int\)7>' ;;
     replay_kernel_7_4) RX='regex:replay_kernel<\(int\)7, \(int\)4>' ;;
+    replay_kernel_7_4_0) RX='regex:replay_kernel<\(int\)7, \(int\)4, \(int\)0>' ;;
     *) RX="regex:$K" ;;
   esac
   timeout 900 $N -k "$RX" -s ${SKIP:-12} -c 1 -o gpurun_out/prof_${K}_${TAG} $B > gpurun_out/ncu_${K}_${TAG}.log 2>&1; echo $K rc=$?

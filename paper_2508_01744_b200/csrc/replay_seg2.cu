@@ -127,16 +127,20 @@ __device__ __forceinline__ double stree(double *buf, int l, bool h0, int k0, dou
     return s;
 }
 
-// b of both slots is staged in shared memory next to A⁻¹ when it fits at 4 blocks per SM
-// (G ≥ 8): its read-modify-write in the Sherman–Morrison step is on the serial chain, and a
-// global-memory round trip there stalled the warp (ncu source attribution)
+// b of both slots is staged in shared memory next to A⁻¹: its read-modify-write in the
+// Sherman–Morrison step is on the serial chain, and a global-memory round trip there stalled the
+// warp (ncu source attribution).  For G = 4 (eight tree buffers per warp) it fits
+// at 4 blocks per SM only if the per-arm ENV-R constants are read through L1 instead of staged.
 template <int G>
-__host__ __device__ constexpr bool b_in_smem() { return G >= 8; }
+__host__ __device__ constexpr bool b_in_smem() { return true; }
+template <int G>
+__host__ __device__ constexpr bool env_in_smem() { return G >= 8; }
 
 template <int G>
 constexpr size_t seg2_smem_bytes(int P, int D)
 {
-    return (3 * kMaxArms + (size_t)kSeg2Warps * 2 * P * 32 + (size_t)kSeg2Warps * (32 / G) * tree_stride<G>()) * 8 +
+    return ((env_in_smem<G>() ? 3 * kMaxArms : 0) + (size_t)kSeg2Warps * 2 * P * 32 +
+            (size_t)kSeg2Warps * (32 / G) * tree_stride<G>()) * 8 +
            (size_t)kSeg2Warps * (32 / G) * sizeof(agft_tuner_stats) +
            (b_in_smem<G>() ? (size_t)kSeg2Warps * 2 * D * 32 * 8 : 0);
 }
@@ -150,16 +154,19 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
     constexpr int E = kWindow / G;
     constexpr int NSEG = 32 / G;
     extern __shared__ double sm[];
+    constexpr bool kEnvS = env_in_smem<G>();
     double *s_dec = sm, *s_pre = sm + kMaxArms, *s_pw = sm + 2 * kMaxArms;
-    double *s_A = sm + 3 * kMaxArms;                                   // [warp][slot][P][32]
+    double *s_A = sm + (kEnvS ? 3 * kMaxArms : 0);                     // [warp][slot][P][32]
     double *s_tree = s_A + kSeg2Warps * 2 * P * 32;                    // [warp][seg][tree_stride]
     agft_tuner_stats *s_st = reinterpret_cast<agft_tuner_stats *>(s_tree + kSeg2Warps * NSEG * tree_stride<G>());
     double *s_B = reinterpret_cast<double *>(s_st + kSeg2Warps * NSEG);  // [warp][slot][D][32] (G ≥ 8)
     const EnvConsts *ec = a.w.env;
-    for (int q = threadIdx.x; q < kMaxArms; q += blockDim.x) {
-        s_dec[q] = ec->dec[q];
-        s_pre[q] = ec->pre[q];
-        s_pw[q] = ec->pw[q];
+    if (kEnvS) {
+        for (int q = threadIdx.x; q < kMaxArms; q += blockDim.x) {
+            s_dec[q] = ec->dec[q];
+            s_pre[q] = ec->pre[q];
+            s_pw[q] = ec->pw[q];
+        }
     }
     for (int q = threadIdx.x; q < kSeg2Warps * NSEG * tree_stride<G>(); q += blockDim.x) s_tree[q] = 0.0;
     __syncthreads();
@@ -358,7 +365,9 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
         }
 
         // ---- a7: response
-        const Response o = env_response(s_dec[kstar], s_pre[kstar], s_pw[kstar], __ldg(&rc->I), __ldg(&rc->P),
+        const Response o = env_response(kEnvS ? s_dec[kstar] : __ldg(&ec->dec[kstar]),
+                                        kEnvS ? s_pre[kstar] : __ldg(&ec->pre[kstar]),
+                                        kEnvS ? s_pw[kstar] : __ldg(&ec->pw[kstar]), __ldg(&rc->I), __ldg(&rc->P),
                                         g, __ldg(&rc->invIm), __ldg(&rc->invAm), wIm,
                                         __ldg(&rc->nT), __ldg(&rc->nE), invW, q_over, a.u_max, a.u_floor,
                                         a.p_idle, a.W);

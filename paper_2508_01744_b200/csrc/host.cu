@@ -357,21 +357,32 @@ static agft_status run_steps(agft_handle h, const void *d_records, uint32_t t0, 
         uint32_t len = sub_chunk(t);
         if (len > n - s) len = n - s;
         else if (n - s - len < len / 2) len = n - s;   // absorb a short tail: one launch wave-tail less (A/B −2%)
+        // refinement on the class schedule (ENV.md §4.11): sub-chunks end at the refinement points
+        // ((t + 1) % period == 0), where a separate pass re-windows every tuner's action space;
+        // the phase-triggered refinements and the closed loop keep the WIDE schedule
+        const bool defer = c.refine.enable && !c.phase.enable && !c.closed.enable &&
+                           c.kernel_policy != AGFT_POLICY_WIDE;
+        if (defer) {
+            const uint32_t to_point = c.refine.period - (t % c.refine.period);
+            if (len > to_point) len = to_point;
+        }
         ReplayArgs a = replay_args(h, d_records, t, len);
         a.rec_stride = n;
         a.rec_off = s;
+        a.rf_defer = defer ? 1u : 0u;
         a.traj = c.record_slots ? traj : nullptr;
         a.gap = c.record_slots ? gap : nullptr;
         a.chosen = chosen;
         a.raw = raw;
         cudaError_t e = cudaSuccess;
-        // refinement re-admits arms, so a tuner's class can grow: one warp per tuner throughout
-        if (c.kernel_policy == AGFT_POLICY_WIDE || c.refine.enable) {
+        // refinement re-admits arms, so a tuner's class can grow: without the deferred pass, one
+        // warp per tuner throughout
+        if (c.kernel_policy == AGFT_POLICY_WIDE || (c.refine.enable && !defer)) {
             e = launch_replay(a, c.d, h->stream);
         } else {
             // MSEG and LANE implement neither the exploitation phase (ENV.md §4.10) nor the closed
             // loop (§6): AUTO (SOLO / SEG2 / WIDE) instead
-            const bool ext = c.phase.enable || c.closed.enable;
+            const bool ext = c.phase.enable || c.closed.enable || defer;   // (+ deferred refinement)
             const bool split = c.kernel_policy != AGFT_POLICY_MSEG || ext;
             const bool lane = c.kernel_policy == AGFT_POLICY_LANE && lane_supported(c.d) && !ext;
             a.force_exact = lane_force_exact();
@@ -395,6 +406,12 @@ static agft_status run_steps(agft_handle h, const void *d_records, uint32_t t0, 
                 if (e == cudaSuccess) e = cudaEventRecord(h->join[k], h->side[k]);
                 if (e == cudaSuccess) e = cudaStreamWaitEvent(h->stream, h->join[k], 0);
             }
+        }
+        if (e == cudaSuccess && defer && (t + len) % c.refine.period == 0u) {
+            ReplayArgs r = replay_args(h, d_records, t + len - 1, 1);   // as of the sub-chunk's last step
+            r.rec_stride = n;
+            r.rec_off = s + len - 1;
+            e = launch_refine(r, c.d, h->stream);
         }
         if (e != cudaSuccess) return cuda_status(h, e);
         s += len;

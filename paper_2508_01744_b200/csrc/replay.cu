@@ -170,7 +170,7 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
     }
     double wlo = 0.0, whi = 0.0, rlo = 0.0, rhi = 0.0;
     uint32_t wcount = 0u, whead = 0u;
-    if (MODE != 1) {                                  // select never touches the EDP window
+    if (MODE != 1 && MODE != 3) {                     // select / refine never touch the EDP window
         wlo = a.w.wsorted[tb * kWindow + 2 * lane];
         whi = a.w.wsorted[tb * kWindow + 2 * lane + 1];
         rlo = a.w.wring[tb * kWindow + 2 * lane];
@@ -190,12 +190,80 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
     }
     double *bglob = a.w.b + tb * D * kMaxArms;
 
+    // ENV.md §4.11 mixed maturity-based refinement as of step t at context x (after pruning)
+    auto refine = [&](uint32_t t, const double (&x)[D]) {
+        int anchor = -1;
+        if (t < a.rf_mature) {                    // Statistical: lowest ē among n ≥ min, not Extreme
+            double be = kInf;
+            int bk2 = 0x7fffffff;
+#pragma unroll
+            for (int j = 0; j < S; ++j) {
+                const int k = 32 * j + lane;
+                if (k < (int)K && !((extb >> j) & 1u) && n[j] >= a.rf_min_samples && ebar[j] < be) {
+                    be = ebar[j];
+                    bk2 = k;
+                }
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                const double ob = __shfl_xor_sync(kFull, be, off);
+                const int ok = __shfl_xor_sync(kFull, bk2, off);
+                if (ob < be || (ob == be && ok < bk2)) { be = ob; bk2 = ok; }
+            }
+            anchor = bk2 == 0x7fffffff ? -1 : bk2;
+        } else {                                  // Predictive: UCB argmax at x_t (Eq. 1's α_t)
+            const double au = alpha_t(prm.alpha0, t, 1.0 / a.tau);
+            double wv[P];
+            {
+                int e = 0;
+#pragma unroll
+                for (int r0 = 0; r0 < D; ++r0)
+#pragma unroll
+                    for (int c = r0; c < D; ++c, ++e) wv[e] = (r0 == c) ? x[r0] * x[r0] : 2.0 * x[r0] * x[c];
+            }
+            double bu = -kInf;
+            int bk2 = 0x7fffffff;
+#pragma unroll
+            for (int j = 0; j < S; ++j) {
+                if ((act >> j) & 1u) {
+                    const double *Aj = sA + j * aJ + lane;
+                    const double *Tj = sT + j * tJ + lane;
+                    const double q = quad_form<P>(wv, Aj, aS);
+                    double p = 0.0;
+#pragma unroll
+                    for (int i = 0; i < D; ++i) p = fma(Tj[i * aS], x[i], p);
+                    const double u = p + au * sqrt(fmax(q, 0.0));
+                    if (u > bu) { bu = u; bk2 = 32 * j + lane; }
+                }
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                const double ob = __shfl_xor_sync(kFull, bu, off);
+                const int ok = __shfl_xor_sync(kFull, bk2, off);
+                if (ob > bu || (ob == bu && ok < bk2)) { bu = ob; bk2 = ok; }
+            }
+            anchor = bk2 == 0x7fffffff ? -1 : bk2;
+        }
+        if (anchor >= 0) {
+#pragma unroll
+            for (int j = 0; j < S; ++j) {
+                const int k = 32 * j + lane;
+                const uint32_t dist = (uint32_t)(k > anchor ? k - anchor : anchor - k) * a.f_step_mhz;
+                const bool in = k < (int)K && dist <= a.rf_half_mhz && dist % a.rf_step_mhz == 0u &&
+                                !((extb >> j) & 1u);
+                act = in ? (act | (1u << j)) : (act & ~(1u << j));
+            }
+            st.n_refine += 1u;
+            st.last_anchor = (uint32_t)anchor;
+        }
+    };
+
     for (uint32_t s = 0; s < a.n_steps; ++s) {
         const uint32_t t = a.t0 + s;
         double x[D];
         double g = 0.0, invIm = 0.0, invAm = 0.0, wIm = 0.0, nT = 0.0, nE = 0.0, baseE = 0.0, baseEDP = 0.0;
         uint32_t recI = 0u, recP = 0u, arr_cl = 0u;
-        if constexpr (MODE == 0) {
+        if constexpr (MODE == 0 || MODE == 3) {
             const StepRec &rec = rp[s];
             if (s + 1 < a.n_steps && lane == 0) {
                 prefetch_l1(&rp[s + 1]);
@@ -226,6 +294,10 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
         } else {                                      // live observe: the x_t of the selection
 #pragma unroll
             for (int i = 0; i < D; ++i) x[i] = a.w.live[tb].x[i];
+        }
+        if constexpr (MODE == 3) {                    // the deferred refinement pass: nothing else
+            refine(t, x);
+            continue;
         }
 
         int nact = 0;
@@ -518,73 +590,10 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
             }
         }
 
-        // ---- ENV.md §4.11 mixed maturity-based refinement (after pruning)
-        if (a.rf_enable && ((t + 1u) % a.rf_period == 0u || (a.ph_enable && phase != phase_sel))) {
-            int anchor = -1;
-            if (t < a.rf_mature) {                    // Statistical: lowest ē among n ≥ min, not Extreme
-                double be = kInf;
-                int bk2 = 0x7fffffff;
-#pragma unroll
-                for (int j = 0; j < S; ++j) {
-                    const int k = 32 * j + lane;
-                    if (k < (int)K && !((extb >> j) & 1u) && n[j] >= a.rf_min_samples && ebar[j] < be) {
-                        be = ebar[j];
-                        bk2 = k;
-                    }
-                }
-#pragma unroll
-                for (int off = 16; off > 0; off >>= 1) {
-                    const double ob = __shfl_xor_sync(kFull, be, off);
-                    const int ok = __shfl_xor_sync(kFull, bk2, off);
-                    if (ob < be || (ob == be && ok < bk2)) { be = ob; bk2 = ok; }
-                }
-                anchor = bk2 == 0x7fffffff ? -1 : bk2;
-            } else {                                  // Predictive: UCB argmax at x_t (Eq. 1's α_t)
-                const double au = alpha_t(prm.alpha0, t, 1.0 / a.tau);
-                double wv[P];
-                {
-                    int e = 0;
-#pragma unroll
-                    for (int r0 = 0; r0 < D; ++r0)
-#pragma unroll
-                        for (int c = r0; c < D; ++c, ++e) wv[e] = (r0 == c) ? x[r0] * x[r0] : 2.0 * x[r0] * x[c];
-                }
-                double bu = -kInf;
-                int bk2 = 0x7fffffff;
-#pragma unroll
-                for (int j = 0; j < S; ++j) {
-                    if ((act >> j) & 1u) {
-                        const double *Aj = sA + j * aJ + lane;
-                        const double *Tj = sT + j * tJ + lane;
-                        const double q = quad_form<P>(wv, Aj, aS);
-                        double p = 0.0;
-#pragma unroll
-                        for (int i = 0; i < D; ++i) p = fma(Tj[i * aS], x[i], p);
-                        const double u = p + au * sqrt(fmax(q, 0.0));
-                        if (u > bu) { bu = u; bk2 = 32 * j + lane; }
-                    }
-                }
-#pragma unroll
-                for (int off = 16; off > 0; off >>= 1) {
-                    const double ob = __shfl_xor_sync(kFull, bu, off);
-                    const int ok = __shfl_xor_sync(kFull, bk2, off);
-                    if (ob > bu || (ob == bu && ok < bk2)) { bu = ob; bk2 = ok; }
-                }
-                anchor = bk2 == 0x7fffffff ? -1 : bk2;
-            }
-            if (anchor >= 0) {
-#pragma unroll
-                for (int j = 0; j < S; ++j) {
-                    const int k = 32 * j + lane;
-                    const uint32_t dist = (uint32_t)(k > anchor ? k - anchor : anchor - k) * a.f_step_mhz;
-                    const bool in = k < (int)K && dist <= a.rf_half_mhz && dist % a.rf_step_mhz == 0u &&
-                                    !((extb >> j) & 1u);
-                    act = in ? (act | (1u << j)) : (act & ~(1u << j));
-                }
-                st.n_refine += 1u;
-                st.last_anchor = (uint32_t)anchor;
-            }
-        }
+        // ---- ENV.md §4.11 mixed maturity-based refinement (after pruning); on the class schedule
+        // a separate pass (MODE 3) applies it at the sub-chunk end instead (rf_defer)
+        if (a.rf_enable && !a.rf_defer && ((t + 1u) % a.rf_period == 0u || (a.ph_enable && phase != phase_sel)))
+            refine(t, x);
 
         // ---- a11: stats (ENV.md §4.9 order) and trajectory record
         st.sum_energy = xadd(st.sum_energy, E);
@@ -640,16 +649,20 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
         a.w.clq[tb * 2] = clq;
         a.w.clq[tb * 2 + 1] = clqb;
     }
-    a.w.wsorted[tb * kWindow + 2 * lane] = wlo;
-    a.w.wsorted[tb * kWindow + 2 * lane + 1] = whi;
-    a.w.wring[tb * kWindow + 2 * lane] = rlo;
-    a.w.wring[tb * kWindow + 2 * lane + 1] = rhi;
+    if (MODE != 3) {
+        a.w.wsorted[tb * kWindow + 2 * lane] = wlo;
+        a.w.wsorted[tb * kWindow + 2 * lane + 1] = whi;
+        a.w.wring[tb * kWindow + 2 * lane] = rlo;
+        a.w.wring[tb * kWindow + 2 * lane + 1] = rhi;
+    }
     int nact_end = 0;
 #pragma unroll
     for (int j = 0; j < S; ++j) nact_end += popc_ballot((act >> j) & 1u);
     if (lane == 0) {
-        a.w.wmeta[tb * 2] = wcount;
-        a.w.wmeta[tb * 2 + 1] = whead;
+        if (MODE != 3) {
+            a.w.wmeta[tb * 2] = wcount;
+            a.w.wmeta[tb * 2 + 1] = whead;
+        }
         st.n_active = (uint32_t)nact_end;
         if (a.ph_enable) {
             a.w.ph[tb] = s_ph[warp];
@@ -712,5 +725,7 @@ cudaError_t launch_live(const ReplayArgs &a, uint32_t D, int mode, cudaStream_t 
 {
     return mode == 1 ? launch_mode<1>(a, D, s) : launch_mode<2>(a, D, s);
 }
+
+cudaError_t launch_refine(const ReplayArgs &a, uint32_t D, cudaStream_t s) { return launch_mode<3>(a, D, s); }
 
 }  // namespace agft

@@ -482,6 +482,10 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
                     }
                     nact -= ce + ch + cc;
                 }
+                if (a.rf_enable) {                    // ENV.md §4.11: Extreme removals stay out for good
+                    if (rm0 && ext0) atomicOr(a.w.extm + (size_t)tb * 4 + (key0 >> 5), 1u << (key0 & 31));
+                    if (rm1 && ext1) atomicOr(a.w.extm + (size_t)tb * 4 + (key1 >> 5), 1u << (key1 & 31));
+                }
                 if (rm0) {
                     act0 = false;
                     tree[tslot<G>(key0)] = 0.0;       // keep the tree buffer's non-Q slots at +0.0

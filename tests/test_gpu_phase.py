@@ -64,7 +64,8 @@ def test_c4_sweep_with_phase_sampled():
     assert (st["exploit_steps"] > 0).mean() > 0.5
 
 
-# ---------------------------------------------------------------- ENV.md §4.11 refinement (WIDE schedule)
+# ------------------------------------------- ENV.md §4.11 refinement: WIDE (policy 1) and the class schedule
+# with the deferred refinement pass at sub-chunk ends (policy 0 without the phase switch)
 @pytest.mark.parametrize("kw", [
     dict(rf_enable=1),                                               # C2 defaults: statistical → predictive
     dict(rf_enable=1, ph_enable=1),                                  # + refinement on phase transitions
@@ -72,16 +73,29 @@ def test_c4_sweep_with_phase_sampled():
     dict(rf_enable=1, ext_round_limit=200, ext_min_samples=1),       # many Extreme removals (permanent)
     dict(rf_enable=1, n_arms=35, f_step_mhz=45, rf_half_mhz=225, rf_step_mhz=45),
 ])
-def test_refinement_parity(kw):
+@pytest.mark.parametrize("policy", [0, 1])
+def test_refinement_parity(kw, policy):
     cfg = named_config("C2")
     cfg.update(n_tuners=5, n_traces=5, T=1500, ph_enable=0)
     cfg.update(kw)
     ids = list(range(5))
     params = tuner_params(cfg, ids)
     params["alpha0"] = np.array([0.0, 0.3, 1.0, 2.0, 5.0])
-    tb, params, st, traj, _ = _run(cfg, 1500, params=params, record=ids, chunk=512, policy=0)
+    tb, params, st, traj, _ = _run(cfg, 1500, params=params, record=ids, chunk=512, policy=policy)
     _check(cfg, tb, params, st, ids, 1500, traj)
     assert np.all(st["n_refine"] > 0)
+
+
+def test_refinement_c4_sample_class_schedule():
+    """Refinement without the phase switch on the class schedule (deferred pass), C4 trace 0's
+    256 tuners for 6,000 windows, a sample checked against the oracle."""
+    cfg = named_config("C4")
+    cfg.update(n_traces=1, rf_enable=1)
+    ids = list(range(256))
+    params = tuner_params(cfg, ids)
+    sample = [0, 5, 31, 64, 130, 200, 255]
+    tb, params, st, traj, _ = _run(cfg, 6000, params=params, record=sample, chunk=4500)
+    _check(cfg, tb, params, st, sample, 6000, traj)
 
 
 def test_refinement_c4_sample():

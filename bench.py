@@ -182,9 +182,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--closed", action="store_true",
-                    help="ENV-C closed-loop environment (ENV.md §6; WIDE schedule, raw rows alongside the records)")
+                    help="ENV-C closed-loop environment (ENV.md §6; raw rows alongside the records)")
     ap.add_argument("--refine", action="store_true",
-                    help="enable mixed maturity-based refinement (ENV.md §4.11; WIDE schedule)")
+                    help="enable mixed maturity-based refinement (ENV.md §4.11; class schedule + refinement passes)")
     ap.add_argument("--chunk", type=int, default=CHUNK, help="windows per agft_replay call (records buffer)")
     ap.add_argument("--phase", action="store_true",
                     help="enable the Page-Hinkley exploitation phase (ENV.md §4.10; not the §8(a) headline)")
@@ -212,9 +212,9 @@ def main():
     if args.phase:
         cfg["ph_enable"] = 1          # ENV.md §4.10 exploitation phase
     if args.refine:
-        cfg["rf_enable"] = 1          # ENV.md §4.11 refinement (NEXT row 1; WIDE schedule)
+        cfg["rf_enable"] = 1          # ENV.md §4.11 refinement (NEXT row 1)
     if args.closed:
-        cfg["cl_enable"] = 1          # ENV.md §6 closed loop (NEXT row 3; WIDE schedule)
+        cfg["cl_enable"] = 1          # ENV.md §6 closed loop (NEXT row 3)
     T = cfg["T"]
 
     if args.impl == "reference":

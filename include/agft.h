@@ -97,13 +97,14 @@ typedef struct { uint32_t enable, window; double delta, lambda; } agft_phase;
 /* Mixed maturity-based refinement (ENV.md §4.11): every `period` rounds
  * (and on a phase transition) the action space becomes the ±half_mhz window on the step_mhz
  * lattice around an anchor — the lowest-mean-EDP arm with ≥ min_samples observations while
- * t < mature, the UCB argmax after — minus Extreme-pruned arms.  Runs on the WIDE schedule. */
+ * t < mature, the UCB argmax after — minus Extreme-pruned arms.  Without the phase switch it runs on
+ * the class schedule with a refinement pass at every period end; with it, on the WIDE schedule. */
 typedef struct { uint32_t enable, period, mature, min_samples, half_mhz, step_mhz; } agft_refine;
 
 /* ENV-C closed loop (ENV.md §6): requests a window cannot
  * serve at the chosen clock (u > 1) wait into the next window, where the snapshot sees them
  * (x1, the concurrency penalty, TTFT); the f_max baseline carries its own backlog.  q_max caps
- * the backlog (requests).  Needs the raw rows: replay with agft_replay_raw.  WIDE schedule. */
+ * the backlog (requests).  Needs the raw rows: replay with agft_replay_raw. */
 typedef struct { uint32_t enable, q_max; } agft_closed;
 
 typedef struct {

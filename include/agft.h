@@ -173,6 +173,15 @@ size_t agft_workspace_bytes(const agft_config *cfg);
 agft_status agft_create(const agft_config *cfg, const agft_tuner_params *d_params,
                         void *d_workspace, size_t ws_bytes, void *stream, agft_handle *out);
 
+/* Checkpoint / resume ("state can be exported for checkpoint and analysis").  Every tuner's
+ * state lives in the caller's workspace, so a checkpoint is the caller's copy of the workspace bytes
+ * plus the step counter (agft_get_step) and the sweep counter; agft_attach builds a handle on a
+ * workspace that already holds such a state (validating cfg exactly as agft_create does, touching
+ * no tuner state) and sets the counters to t and sweep_t.  A workspace copied from a handle with the
+ * same cfg resumes bit-identically. */
+agft_status agft_attach(const agft_config *cfg, void *d_workspace, size_t ws_bytes, void *stream, uint32_t t,
+                        uint32_t sweep_t, agft_handle *out);
+
 /* Re-initialise every tuner of the handle (as agft_create does, keeping its params)
  * and set the step counter to 0.  Asynchronous. */
 agft_status agft_reset(agft_handle h);

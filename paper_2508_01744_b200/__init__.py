@@ -19,7 +19,7 @@ from ._abi import (NO_RECORD, PARAMS_DTYPE, RECORD_BYTES, ROW_WORDS, STATS_DTYPE
                    make_config, make_params)
 
 __all__ = ["agft_workspace_bytes", "agft_create", "agft_reset", "agft_trace_generate", "agft_step", "agft_replay",
-           "agft_select", "agft_observe", "agft_replay_raw",
+           "agft_select", "agft_observe", "agft_replay_raw", "agft_attach",
            "agft_stats", "agft_export_arms", "agft_get_step", "agft_run", "agft_sweep", "agft_regret",
            "agft_destroy", "SweepSums",
            "TunerBatch", "record_slot_count", "make_config", "make_params", "PARAMS_DTYPE", "STATS_DTYPE", "NO_RECORD",
@@ -55,6 +55,14 @@ def agft_create(cfg_c, d_params, workspace, stream=None) -> int:
     _abi.check("agft_create", _abi.lib().agft_create(C.byref(cfg_c), _p(d_params), _p(workspace),
                                                       workspace.numel() * workspace.element_size(),
                                                       _stream(stream), C.byref(h)))
+    return h.value
+
+
+def agft_attach(cfg_c, workspace, t, sweep_t=0, stream=None) -> int:
+    h = C.c_void_p()
+    _abi.check("agft_attach", _abi.lib().agft_attach(C.byref(cfg_c), _p(workspace),
+                                                      workspace.numel() * workspace.element_size(),
+                                                      _stream(stream), t, sweep_t, C.byref(h)))
     return h.value
 
 
@@ -173,6 +181,32 @@ class TunerBatch:
 
     def reset(self):
         agft_reset(self.h)
+
+    def checkpoint(self):
+        """(workspace bytes on the host, step counter): everything a resume needs."""
+        import torch
+        torch.cuda.synchronize(self.device)
+        return self.workspace.cpu(), self.t
+
+    @classmethod
+    def resume(cls, cfg: dict, params: dict, state, device="cuda", trace_base: int = 0, n_traces=None,
+               record_slot=None, policy: int = 0):
+        """A TunerBatch on a copy of a checkpointed workspace, continuing at its step counter."""
+        import torch
+        self = cls.__new__(cls)
+        self.cfg = cfg
+        self.device = torch.device(device)
+        self.n = len(params["trace_id"])
+        self.n_traces = cfg["n_traces"] if n_traces is None else n_traces
+        self.record_slots = record_slot_count(record_slot)
+        self.cfg_c = make_config(cfg, n_tuners=self.n, n_traces=self.n_traces, trace_base=trace_base,
+                                 record_slots=self.record_slots, policy=policy)
+        ws_host, t = state
+        self.workspace = ws_host.to(self.device)
+        self.d_params = None
+        self.stream = None
+        self.h = agft_attach(self.cfg_c, self.workspace, t)
+        return self
 
     @property
     def t(self) -> int:

@@ -99,6 +99,7 @@ PROTOTYPES = {
     "agft_workspace_bytes": (C.c_size_t, [C.POINTER(AgftConfig)]),
     "agft_create": (C.c_int, [C.POINTER(AgftConfig), vp, vp, C.c_size_t, vp, C.POINTER(vp)]),
     "agft_reset": (C.c_int, [vp]),
+    "agft_attach": (C.c_int, [C.POINTER(AgftConfig), vp, C.c_size_t, vp, u32, u32, C.POINTER(vp)]),
     "agft_trace_generate": (C.c_int, [vp, u32, u32, vp, vp]),
     "agft_step": (C.c_int, [vp, vp, vp]),
     "agft_select": (C.c_int, [vp, vp, vp]),

@@ -105,6 +105,29 @@ void destroy_streams(agft_handle h)
     if (h->fork) cudaEventDestroy(h->fork);
 }
 
+// Class streams by priority: the multi-wave SEG classes first, so the block scheduler fills
+// SMs longest-work-first and the short classes pack around them (A/B: −2.3% per C4 day,
+// DESIGN.md §4).  AGFT_STREAM_PRIO=0 disables; AGFT_PRIO_ORDER="2,1,3,0,5,4" overrides the
+// order (class ids of agft_internal.cuh, highest priority first).
+cudaError_t create_streams(agft_handle h)
+{
+    cudaError_t e = cudaEventCreateWithFlags(&h->fork, cudaEventDisableTiming);
+    int prio_lo = 0, prio_hi = 0;
+    const bool prio = stream_prio_enabled() && cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi) == cudaSuccess;
+    int rank[kNumCls];
+    prio_order(rank);
+    for (int c = 0; c < kNumCls && e == cudaSuccess; ++c) {
+        int p = prio_lo;
+        if (prio) {
+            p = prio_hi + rank[c];
+            if (p > prio_lo) p = prio_lo;
+        }
+        e = cudaStreamCreateWithPriority(&h->side[c], cudaStreamNonBlocking, p);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->join[c], cudaEventDisableTiming);
+    }
+    return e;
+}
+
 agft_status validate(const agft_config *c)
 {
     if (!c) return AGFT_E_INVALID_ARG;
@@ -277,30 +300,52 @@ agft_status agft_create(const agft_config *cfg, const agft_tuner_params *d_param
         h->join[c] = nullptr;
     }
 
-    cudaError_t e = cudaEventCreateWithFlags(&h->fork, cudaEventDisableTiming);
-    // Class streams by priority: the multi-wave SEG classes first, so the block scheduler fills
-    // SMs longest-work-first and the short classes pack around them (A/B: −2.3% per C4 day,
-    // DESIGN.md §4).  AGFT_STREAM_PRIO=0 disables; AGFT_PRIO_ORDER="2,1,3,0,5,4" overrides the
-    // order (class ids of agft_internal.cuh, highest priority first).
-    int prio_lo = 0, prio_hi = 0;
-    const bool prio = stream_prio_enabled() && cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi) == cudaSuccess;
-    int rank[kNumCls];
-    prio_order(rank);
-    for (int c = 0; c < kNumCls && e == cudaSuccess; ++c) {
-        int p = prio_lo;
-        if (prio) {
-            p = prio_hi + rank[c];
-            if (p > prio_lo) p = prio_lo;
-        }
-        e = cudaStreamCreateWithPriority(&h->side[c], cudaStreamNonBlocking, p);
-        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->join[c], cudaEventDisableTiming);
-    }
+    cudaError_t e = create_streams(h);
     if (e == cudaSuccess)
         e = cudaMemcpyAsync(h->ws.params, d_params, sizeof(agft_tuner_params) * cfg->n_tuners,
                             cudaMemcpyDeviceToDevice, h->stream);
     if (e == cudaSuccess) e = launch_init(h->ws, *cfg, h->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
     if (e != cudaSuccess) {
+        destroy_streams(h);
+        delete h;
+        return AGFT_E_CUDA;
+    }
+    *out = h;
+    return AGFT_OK;
+}
+
+agft_status agft_attach(const agft_config *cfg, void *d_workspace, size_t ws_bytes, void *stream, uint32_t t,
+                        uint32_t sweep_t, agft_handle *out)
+{
+    if (!out) return AGFT_E_INVALID_ARG;
+    *out = nullptr;
+    agft_status st = validate(cfg);
+    if (st != AGFT_OK) return st;
+    if (!d_workspace) return AGFT_E_INVALID_ARG;
+    if (reinterpret_cast<uintptr_t>(d_workspace) % 256 != 0) return AGFT_E_WORKSPACE;
+    const Layout L = make_layout(cfg->n_tuners, cfg->d);
+    if (ws_bytes < L.total) return AGFT_E_WORKSPACE;
+    int dev = 0, major = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return AGFT_E_DEVICE;
+    if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess) return AGFT_E_DEVICE;
+    if (major != 10) return AGFT_E_DEVICE;
+    agft_handle h = new (std::nothrow) agft_handle_s;
+    if (!h) return AGFT_E_INVALID_ARG;
+    h->cfg = *cfg;
+    h->layout = L;
+    h->ws = make_ws(d_workspace, L);
+    h->stream = static_cast<cudaStream_t>(stream);
+    h->t = t;
+    h->sweep_t = sweep_t;
+    h->live_pending = 0;
+    h->sticky = AGFT_OK;
+    h->fork = nullptr;
+    for (int c = 0; c < kNumCls; ++c) {
+        h->side[c] = nullptr;
+        h->join[c] = nullptr;
+    }
+    if (create_streams(h) != cudaSuccess) {
         destroy_streams(h);
         delete h;
         return AGFT_E_CUDA;

@@ -149,7 +149,8 @@ def run_cpu_baseline(cfg: dict, n_tuners: int, T: int) -> dict:
     ost = oracle.run_batch(cfg, params, T, threads=cores)
     dt = time.perf_counter() - t
     return {"value": n_tuners * T / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"{cfg.get('name', 'C4')} tuners 0..{n_tuners - 1} (trace 0, all 256 hyper-parameter points) × {T} steps, "
+            "sample": f"{cfg.get('name', 'C4')} tuners 0..{n_tuners - 1}"
+                      f"{' (trace 0, all 256 hyper-parameter points)' if cfg.get('sweep') == 'hyper256' else ''} × {T} steps, "
                       f"free-running, {dt:.1f} s on {cores} threads"}, ost
 
 
@@ -162,7 +163,7 @@ def parity_summary(gst, ost) -> dict:
     (same config, same windows): trajectory-hash matches and, for those, exact equality of every
     counter and fp64 sum (ENV.md §0).  A free-running oracle may leave the GPU's path at a near-tie
     (ENV.md §4.5); the GPU's near-tie count is reported beside it."""
-    n = len(ost)
+    n = min(len(ost), len(gst))
     match = [i for i in range(n) if int(gst["traj_hash"][i]) == ost[i]["traj_hash"]]
     exact = [i for i in match if all(gst[f][i] == ost[i][f] for f in PARITY_EXACT)]
     return {"tuners": n, "traj_hash_match": len(match), "stats_exact_given_traj": len(exact),
@@ -331,7 +332,8 @@ def main():
            "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": {"workload": f"{args.config}: {n} tuners/GPU × {cfg['n_arms']} arms × d={cfg['d']} × "
-                                  f"{T} windows ({R} traces/GPU, α×pruning sweep, diurnal+burst)",
+                                  f"{T} windows ({R} traces/GPU{', α×pruning sweep' if cfg.get('sweep') == 'hyper256' else ''}, "
+                                  f"{['fluctuating', 'diurnal', 'burst', 'fluct/diurnal/burst', 'diurnal+burst'][cfg['pattern_mode']]})",
                       "tuners_per_gpu": n, "T": T, "arms": cfg["n_arms"], "d": cfg["d"],
                       "phase_switch": bool(cfg.get("ph_enable", 0)),
                       "refinement": bool(cfg.get("rf_enable", 0)),
@@ -345,7 +347,7 @@ def main():
     if not args.no_e2e:
         out["e2e"] = e2e_leg(cfg, params, sh.trace_base, world, local, chunk, n, T, args)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"], ost = run_cpu_baseline(cfg, 256, T)
+        out["cpu_baseline"], ost = run_cpu_baseline(cfg, min(256, n), T)
         out["parity"] = parity_summary(st, ost)
     if rank == 0:
         print(json.dumps(out), flush=True)

@@ -132,3 +132,37 @@ def test_record_slot_count():
     r[3], r[7] = 0, 4
     assert pkg.record_slot_count(r) == 5
     assert pkg.record_slot_count(np.arange(6, dtype=np.uint32)) == 6
+
+
+def test_closed_loop_and_attach_host_checks(lib):
+    """ABI v5: agft_closed validation, and agft_attach's host-side checks (no kernel launched)."""
+    import ctypes
+    import numpy as np
+    assert _bad(lib, cl_enable=2) == -1
+    assert _bad(lib, cl_enable=1, cl_q_max=0) == 0            # a zero cap is the open loop (ENV.md §6)
+    c = _abi.make_config(named_config("C2"))
+    h = ctypes.c_void_p()
+    need = pkg.agft_workspace_bytes(c)
+    buf = np.zeros(need + 512, np.uint8)
+    base = (buf.ctypes.data + 255) // 256 * 256
+    assert lib.agft_attach(ctypes.byref(c), base, need - 1, None, 0, 0, ctypes.byref(h)) == -6
+    assert lib.agft_attach(ctypes.byref(c), base + 8, need, None, 0, 0, ctypes.byref(h)) == -6   # misaligned
+    c.abi_version = 99
+    assert lib.agft_attach(ctypes.byref(c), base, need, None, 0, 0, ctypes.byref(h)) == -1
+    assert not h.value
+
+
+def test_bench_parity_summary_counts():
+    """bench.py's in-line parity check: hashes first, then every exact field, on any sample size."""
+    import numpy as np
+    import bench
+    g = np.zeros(3, dtype=_abi.STATS_DTYPE)
+    g["traj_hash"] = [1, 2, 3]
+    g["sum_edp"] = [1.0, 2.0, 3.0]
+    ost = [{f: 0 for f in bench.PARITY_EXACT} for _ in range(2)]
+    for i, o in enumerate(ost):
+        o["traj_hash"] = int(g["traj_hash"][i])
+        o["sum_edp"] = float(g["sum_edp"][i])
+    ost[1]["sum_edp"] = 2.5                                    # same path, different sum
+    p = bench.parity_summary(g, ost)
+    assert p["tuners"] == 2 and p["traj_hash_match"] == 2 and p["stats_exact_given_traj"] == 1

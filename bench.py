@@ -158,6 +158,32 @@ PARITY_EXACT = ("steps", "n_active", "sum_active", "n_pruned_extreme", "n_pruned
                 "sum_energy", "sum_tpot", "sum_ttft", "sum_edp", "sum_reward", "base_energy", "base_edp")
 
 
+def arm_state_errors(cfg, params, tb, T, sample) -> dict:
+    """the largest relative error of A⁻¹ and θ (Sherman–Morrison on the GPU against
+    Gauss–Jordan / solve in the oracle, ENV.md §4.3) over a few tuners of the timed run, and whether
+    their counters and b match exactly; the oracle runs each tuner's full day single-threaded."""
+    import oracle
+    worst_a = worst_t = 0.0
+    exact = 0
+    for i in sample:
+        tu = oracle.make_tuner(int(params["trace_id"][i]), params["alpha0"][i], params["ext_reward_threshold"][i],
+                               params["hist_k"][i])
+        _, oa, _ = oracle.run_tuner(cfg, tu, T=T)
+        g = tb.export_arms(i)
+        for name, key in (("Ainv", "a"), ("theta", "t")):
+            go, oo = np.asarray(g[name]), np.asarray(oa[name])
+            err = float(np.max(np.abs(go - oo) / np.maximum(np.max(np.abs(oo), axis=tuple(range(1, oo.ndim)),
+                                                                    keepdims=True), 1e-300)))
+            if key == "a":
+                worst_a = max(worst_a, err)
+            else:
+                worst_t = max(worst_t, err)
+        exact += int(all(np.array_equal(np.asarray(g[f]).astype(np.float64), np.asarray(oa[f]).astype(np.float64))
+                         for f in ("n", "b", "rbar", "ebar", "active")))
+    return {"arm_state_tuners": list(sample), "ainv_max_rel_err": worst_a, "theta_max_rel_err": worst_t,
+            "arm_counters_b_exact": exact, "arm_state_tolerance": 1e-9}
+
+
 def parity_summary(gst, ost) -> dict:
     """The timed run's own statistics for the tuners the cpu_baseline leg ran through the oracle
     (same config, same windows): trajectory-hash matches and, for those, exact equality of every
@@ -349,6 +375,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"], ost = run_cpu_baseline(cfg, min(256, n), T)
         out["parity"] = parity_summary(st, ost)
+        out["parity"].update(arm_state_errors(cfg, params, tb, T, [i for i in (0, 63, 128, 255) if i < n]))
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:

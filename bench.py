@@ -148,7 +148,12 @@ def run_cpu_baseline(cfg: dict, n_tuners: int, T: int) -> dict:
     t = time.perf_counter()
     ost = oracle.run_batch(cfg, params, T, threads=cores)
     dt = time.perf_counter() - t
+    n1 = min(4, n_tuners)                              # the 1-thread rate beside it
+    t1 = time.perf_counter()
+    oracle.run_batch(cfg, tuner_params(cfg, list(range(n1))), T, threads=1)
+    dt1 = time.perf_counter() - t1
     return {"value": n_tuners * T / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "one_thread_value": n1 * T / dt1, "one_thread_sample": f"tuners 0..{n1 - 1} × {T} steps, 1 thread",
             "sample": f"{cfg.get('name', 'C4')} tuners 0..{n_tuners - 1}"
                       f"{' (trace 0, all 256 hyper-parameter points)' if cfg.get('sweep') == 'hyper256' else ''} × {T} steps, "
                       f"free-running, {dt:.1f} s on {cores} threads"}, ost

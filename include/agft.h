@@ -1,5 +1,5 @@
 /*
- * agft.h — C ABI of the B200-native AGFT hot path (ABI version 1).
+ * agft.h — C ABI of the B200-native AGFT hot path (ABI version AGFT_ABI_VERSION, below).
  *
  * What it computes: a batched replay of N independent AGFT frequency tuners
  * (arXiv 2508.01744 §4), each a contextual LinUCB bandit over a frequency grid,
@@ -30,18 +30,16 @@
 extern "C" {
 #endif
 
-#define AGFT_ABI_VERSION 5u         /* 2: + agft_phase; 3: + agft_refine (and their stats); 4: + agft_select/agft_observe;
-                                       5: + agft_closed / agft_replay_raw */
+#define AGFT_ABI_VERSION 6u         /* 2: + agft_phase; 3: + agft_refine (and their stats); 4: + agft_select/agft_observe;
+                                       5: + agft_closed / agft_replay_raw; 6: MSEG/LANE policies retired */
 #define AGFT_MAX_ARMS 128u          /* K ≤ 128 */
 #define AGFT_MAX_D 7u               /* the paper's 7-dim context */
 #define AGFT_MAX_WINDOW 64u         /* reward-median window, AMB-3 */
 #define AGFT_RECORD_BYTES 128u      /* ENV.md §3.2 per-window step record */
 #define AGFT_ROW_WORDS 12u          /* ENV.md §2.2 raw trace row (uint32) */
 #define AGFT_NO_RECORD 0xFFFFFFFFu  /* agft_tuner_params.record_slot: not recorded */
-#define AGFT_POLICY_AUTO 0u         /* re-classify by active-arm count: SOLO (1), SEG<8/16/32>, WIDE (>32) */
+#define AGFT_POLICY_AUTO 0u         /* re-classify by active-arm count: SOLO (1), SEG<4/8/16/32> (2..64), WIDE (>64) */
 #define AGFT_POLICY_WIDE 1u         /* one warp per tuner for every step (reference schedule) */
-#define AGFT_POLICY_MSEG 2u         /* as AUTO but 2..32 arms on MSEG (arm state streamed from L2) */
-#define AGFT_POLICY_LANE 3u         /* as AUTO but 2..32 arms on LANE (lane per tuner, batched scoring) */
 
 typedef struct agft_handle_s *agft_handle;
 
@@ -114,7 +112,7 @@ typedef struct {
     uint32_t n_traces;        /* R: traces held by this handle (local ids 0..R-1) */
     uint32_t trace_base;      /* global id of local trace 0 (Philox key, ENV.md §1) */
     uint32_t record_slots;    /* rows of d_traj / d_gap in agft_replay (0 = none) */
-    uint32_t kernel_policy;   /* AGFT_POLICY_AUTO, _WIDE, _MSEG or _LANE */
+    uint32_t kernel_policy;   /* AGFT_POLICY_AUTO or AGFT_POLICY_WIDE (anything else: AGFT_E_INVALID_ARG) */
     uint32_t pad0;
     agft_grid grid;
     agft_prune prune;
@@ -132,11 +130,14 @@ typedef struct {
 /* Per-tuner parameters (the hyper-parameter sweep axes of C4/C5). */
 typedef struct {
     uint32_t trace_id;        /* LOCAL trace index in [0, n_traces) */
-    uint32_t record_slot;     /* row of d_traj/d_gap, or AGFT_NO_RECORD */
-    double alpha0;            /* ≥ 0 (0 = greedy, Eq. 2) */
+    uint32_t record_slot;     /* row of d_traj/d_gap (< record_slots), or AGFT_NO_RECORD */
+    double alpha0;            /* finite, ≥ 0 (0 = greedy, Eq. 2) */
     double extreme_reward_threshold; /* τ_E, P:387 (−1.2) */
-    double historical_k;      /* k_h, P:388 (1.0) */
-} agft_tuner_params;          /* 32 B */
+    double historical_k;      /* k_h, P:388 (1.0); finite, ≥ 0 */
+} agft_tuner_params;          /* 32 B.  agft_create / agft_attach / agft_run reject (AGFT_E_INVALID_ARG)
+                                 a trace_id ≥ n_traces, a record_slot that is neither < record_slots
+                                 nor AGFT_NO_RECORD, or a non-finite / negative alpha0, τ_E or k_h
+                                 (τ_E finite, any sign). */
 
 /* Per-tuner statistics (ENV.md §4.9–§4.11), 128 B. */
 typedef struct {
@@ -164,7 +165,10 @@ agft_status agft_validate(const agft_config *cfg);
 uint32_t agft_struct_size(int which);
 
 /* Bytes of device workspace a config needs (0 if the config is invalid). The
- * workspace must be 256-byte aligned. */
+ * workspace must be 256-byte aligned.  It holds every tuner's bandit state — per arm A⁻¹ (packed
+ * upper triangle), θ, b, n, r̄, ē (Eqs. 3–5), the active set F_available
+ * (§4.3), the EDP window of the reward (AMB-3) and the stats —
+ * so that the whole session state is one caller-owned buffer (checkpointable). */
 size_t agft_workspace_bytes(const agft_config *cfg);
 
 /* Validate cfg, lay out d_workspace, copy d_params [n_tuners] into it and initialise
@@ -196,6 +200,7 @@ agft_status agft_trace_generate(agft_handle h, uint32_t t0, uint32_t n_steps, vo
  * at the handle's current step t; d_records = [n_traces][1][128 B] for step t;
  * d_chosen = [n_tuners] chosen arm index, or NULL.  Advances t by 1. */
 agft_status agft_step(agft_handle h, const void *d_records, uint32_t *d_chosen);
+/* (d_chosen of a frozen tuner — stats.flags bit 0 — reads AGFT_NEVER.) */
 
 /* ---- Live two-phase step.  The paper's controller runs one decision
  * per sampling window on a live server (§4): read the window's metrics, pick
@@ -220,8 +225,12 @@ agft_status agft_step(agft_handle h, const void *d_records, uint32_t *d_chosen);
 agft_status agft_select(agft_handle h, const uint32_t *d_rows, uint32_t *d_chosen);
 agft_status agft_observe(agft_handle h, const double *d_resp);
 
-/* n_steps decision windows for every tuner, steps [t0, t0+n_steps); t0 must equal the
- * handle's step counter (AGFT_E_STATE otherwise).  d_records = [n_traces][n_steps][128 B].
+/* The paper's decision loop (§4.2: the context x_t → Eq. 1 arg max over
+ * F_available → execute f_t → reward from the measured EDP → Eqs. 3–5 update of the executed
+ * arm; then §4.3 pruning) run for n_steps consecutive windows of every tuner, fused
+ * into one call: steps [t0, t0+n_steps); t0 must equal the handle's step counter (AGFT_E_STATE
+ * otherwise; AGFT_E_INVALID_ARG on a closed-loop handle or a NULL d_records).
+ * d_records = [n_traces][n_steps][128 B] as agft_trace_generate writes them.
  * d_traj = [record_slots][n_steps] chosen arms and d_gap = [record_slots][n_steps]
  * relative top-2 score gaps (ENV.md §4.5) for tuners with a record_slot; either may be NULL. */
 agft_status agft_replay(agft_handle h, const void *d_records, uint32_t t0, uint32_t n_steps,
@@ -234,10 +243,14 @@ agft_status agft_replay(agft_handle h, const void *d_records, uint32_t t0, uint3
 agft_status agft_replay_raw(agft_handle h, const void *d_records, const uint32_t *d_raw, uint32_t t0,
                             uint32_t n_steps, uint8_t *d_traj, double *d_gap);
 
-/* Copy the per-tuner statistics into d_out [n_tuners]. */
+/* Copy the per-tuner statistics into d_out [n_tuners] (caller-owned device buffer;
+ * asynchronous).  These are the analysis export of SPEC.md:224 and the per-tuner analogues of the
+ * paper's cumulative energy / EDP and mean TTFT / TPOT figures against the f_max default
+ * (Tables 2–3). */
 agft_status agft_stats(agft_handle h, agft_tuner_stats *d_out);
 
-/* One tuner's arm state (for checkpoints and parity): d_ainv_packed [K][d(d+1)/2]
+/* One tuner's arm state (for checkpoints and parity; "bandit state (all arms …)
+ * serializes … for session checkpointing and post-hoc analysis"): d_ainv_packed [K][d(d+1)/2]
  * (row-major upper triangle of A⁻¹), d_b [K][d], d_theta [K][d], d_n [K], d_rbar [K],
  * d_ebar [K], d_active_mask [4] (bit k of word k/32).  Any pointer may be NULL. */
 agft_status agft_export_arms(agft_handle h, uint32_t tuner, double *d_ainv_packed, double *d_b,
@@ -246,6 +259,12 @@ agft_status agft_export_arms(agft_handle h, uint32_t tuner, double *d_ainv_packe
 
 /* The handle's current step counter. */
 agft_status agft_get_step(agft_handle h, uint32_t *t);
+
+/* The counters a checkpoint needs besides the workspace bytes (agft_attach): the step counter t,
+ * the offline-sweep counter sweep_t, and live_pending = 1 between an agft_select and its
+ * agft_observe (a checkpoint taken then would lose the pending selection; callers refuse it).
+ * Any pointer may be NULL. */
+agft_status agft_get_counters(agft_handle h, uint32_t *t, uint32_t *sweep_t, uint32_t *live_pending);
 
 /* End to end from HOST buffers: copies h_params [n_tuners] host→device, creates the
  * tuners in d_workspace, replays steps [0, n_steps) generating the trace in chunks of
@@ -278,7 +297,8 @@ agft_status agft_sweep(agft_handle h, const void *d_records, uint32_t t0, uint32
 /* From the sweep sums: d_koff [n_traces][6] = k_off(r, p) for prototypes p < 5 (0xFF if
  * prototype p never occurred) and k_off(r) at index 5 (smallest index on ties); and, if
  * d_regret is not NULL, d_regret [n_tuners][2] = (sum_edp − Σ EDP at k°, sum_edp −
- * Σ EDP at k_off(r)) for each tuner's current statistics (compare after the same windows). */
+ * Σ EDP at k_off(r)) for each tuner's current statistics (compare after the same windows).
+ * The sweep is open-loop (ENV.md §5): d_regret on a closed-loop handle returns AGFT_E_INVALID_ARG. */
 agft_status agft_regret(agft_handle h, const double *d_S, const double *d_SP, const uint32_t *d_NP,
                         const double *d_O, uint8_t *d_koff, double *d_regret);
 

@@ -20,7 +20,8 @@ from ._abi import (NO_RECORD, PARAMS_DTYPE, RECORD_BYTES, ROW_WORDS, STATS_DTYPE
 
 __all__ = ["agft_workspace_bytes", "agft_create", "agft_reset", "agft_trace_generate", "agft_step", "agft_replay",
            "agft_select", "agft_observe", "agft_replay_raw", "agft_attach",
-           "agft_stats", "agft_export_arms", "agft_get_step", "agft_run", "agft_sweep", "agft_regret",
+           "agft_stats", "agft_export_arms", "agft_get_step", "agft_get_counters", "agft_run", "agft_sweep",
+           "agft_regret",
            "agft_destroy", "SweepSums",
            "TunerBatch", "record_slot_count", "make_config", "make_params", "PARAMS_DTYPE", "STATS_DTYPE", "NO_RECORD",
            "RECORD_BYTES", "ROW_WORDS", "AgftError", "lib_path"]
@@ -44,6 +45,19 @@ def _stream(stream):
     if stream is None:
         stream = torch.cuda.current_stream()
     return stream.cuda_stream
+
+
+def _on_device(fn):
+    """Run a TunerBatch method with its device current: the library launches on the current
+    device and creates its side streams there."""
+    import functools
+
+    @functools.wraps(fn)
+    def wrapped(self, *a, **k):
+        import torch
+        with torch.cuda.device(self.device):
+            return fn(self, *a, **k)
+    return wrapped
 
 
 def agft_workspace_bytes(cfg_c: _abi.AgftConfig) -> int:
@@ -108,6 +122,13 @@ def agft_get_step(h) -> int:
     t = C.c_uint32()
     _abi.check("agft_get_step", _abi.lib().agft_get_step(h, C.byref(t)))
     return t.value
+
+
+def agft_get_counters(h) -> tuple[int, int, int]:
+    """(step counter t, sweep counter, live_pending) of a handle: what a checkpoint stores."""
+    t, sw, lp = C.c_uint32(), C.c_uint32(), C.c_uint32()
+    _abi.check("agft_get_counters", _abi.lib().agft_get_counters(h, C.byref(t), C.byref(sw), C.byref(lp)))
+    return t.value, sw.value, lp.value
 
 
 def agft_sweep(h, records, t0, n_steps, S, SP, NP, O, best=None):
@@ -177,21 +198,30 @@ class TunerBatch:
         host = make_params(params, record_slot)
         self.d_params = torch.from_numpy(host.view(np.uint8)).to(self.device)
         self.stream = stream
-        self.h = agft_create(self.cfg_c, self.d_params, self.workspace, stream)
+        with torch.cuda.device(self.device):
+            self.h = agft_create(self.cfg_c, self.d_params, self.workspace,
+                                 stream if stream is not None else torch.cuda.current_stream(self.device))
 
+    @_on_device
     def reset(self):
         agft_reset(self.h)
 
     def checkpoint(self):
-        """(workspace bytes on the host, step counter): everything a resume needs."""
+        """(workspace bytes on the host, step counter, sweep counter): everything a resume needs
+        (S:224).  The tuner parameters live in the workspace.  Refused between agft_select and its
+        agft_observe (the pending selection is not part of the state a resume restores)."""
         import torch
+        t, sweep_t, pending = agft_get_counters(self.h)
+        if pending:
+            raise AgftError("checkpoint: a live selection is pending (agft_select without agft_observe)", -7)
         torch.cuda.synchronize(self.device)
-        return self.workspace.cpu(), self.t
+        return self.workspace.cpu(), t, sweep_t
 
     @classmethod
     def resume(cls, cfg: dict, params: dict, state, device="cuda", trace_base: int = 0, n_traces=None,
                record_slot=None, policy: int = 0):
-        """A TunerBatch on a copy of a checkpointed workspace, continuing at its step counter."""
+        """A TunerBatch on a copy of a checkpointed workspace, continuing at its step and sweep
+        counters.  The tuner parameters come from the workspace (``params`` only sizes the batch)."""
         import torch
         self = cls.__new__(cls)
         self.cfg = cfg
@@ -201,11 +231,13 @@ class TunerBatch:
         self.record_slots = record_slot_count(record_slot)
         self.cfg_c = make_config(cfg, n_tuners=self.n, n_traces=self.n_traces, trace_base=trace_base,
                                  record_slots=self.record_slots, policy=policy)
-        ws_host, t = state
+        ws_host, t = state[0], state[1]
+        sweep_t = state[2] if len(state) > 2 else 0
         self.workspace = ws_host.to(self.device)
         self.d_params = None
         self.stream = None
-        self.h = agft_attach(self.cfg_c, self.workspace, t)
+        with torch.cuda.device(self.device):
+            self.h = agft_attach(self.cfg_c, self.workspace, t, sweep_t, torch.cuda.current_stream(self.device))
         return self
 
     @property
@@ -216,6 +248,7 @@ class TunerBatch:
         import torch
         return torch.empty((self.n_traces, n_steps, RECORD_BYTES), dtype=torch.uint8, device=self.device)
 
+    @_on_device
     def generate(self, t0: int, n_steps: int, records=None, raw: bool = False):
         import torch
         records = self.new_records(n_steps) if records is None else records
@@ -229,6 +262,7 @@ class TunerBatch:
         """ENV-C closed loop (ENV.md §6): replays need the raw rows (agft_replay_raw)."""
         return bool(self.cfg.get("cl_enable", 0))
 
+    @_on_device
     def replay(self, records, t0: int, n_steps: int, record: bool = False, raw=None):
         import torch
         traj = gap = None
@@ -241,12 +275,14 @@ class TunerBatch:
             agft_replay(self.h, records, t0, n_steps, traj, gap)
         return traj, gap
 
+    @_on_device
     def step(self, records_t):
         import torch
         chosen = torch.empty(self.n, dtype=torch.int32, device=self.device)
         agft_step(self.h, records_t, chosen)
         return chosen
 
+    @_on_device
     def select(self, rows, chosen=None):
         """Live step, first half: rows [n][12] int32 device tensor of MetricsSnapshot counters →
         chosen arm per tuner (int32 [n] device tensor; -1 = frozen tuner)."""
@@ -256,11 +292,13 @@ class TunerBatch:
         agft_select(self.h, rows, chosen)
         return chosen
 
+    @_on_device
     def observe(self, resp):
         """Live step, second half: resp [n][3] float64 device tensor of measured (E J, TPOT s,
         TTFT s) at the selected frequencies."""
         agft_observe(self.h, resp)
 
+    @_on_device
     def run(self, T: int, chunk: int = 4500, record: bool = False):
         """Generate + replay steps [t, T) in chunks; returns recorded traj/gap (host) if asked."""
         import torch
@@ -286,6 +324,7 @@ class TunerBatch:
     def new_sweep(self) -> SweepSums:
         return SweepSums(self.n_traces, self.cfg["n_arms"], self.device)
 
+    @_on_device
     def sweep(self, records, t0: int, n_steps: int, sums: SweepSums, best: bool = False):
         """ENV.md §5 over windows [t0, t0+n_steps) into ``sums``; returns k° [n_traces][n] if asked."""
         import torch
@@ -293,6 +332,7 @@ class TunerBatch:
         agft_sweep(self.h, records, t0, n_steps, sums.S, sums.SP, sums.NP, sums.O, b)
         return b
 
+    @_on_device
     def regret(self, sums: SweepSums):
         """Table-6 Offline arms into ``sums.koff`` and per-tuner (window, fixed) regret [n][2]."""
         import torch
@@ -300,6 +340,7 @@ class TunerBatch:
         agft_regret(self.h, sums.S, sums.SP, sums.NP, sums.O, sums.koff, out)
         return out
 
+    @_on_device
     def stats_tensor(self):
         import torch
         out = torch.empty(self.n * STATS_DTYPE.itemsize, dtype=torch.uint8, device=self.device)
@@ -309,6 +350,7 @@ class TunerBatch:
     def stats(self) -> np.ndarray:
         return self.stats_tensor().cpu().numpy().view(STATS_DTYPE)
 
+    @_on_device
     def export_arms(self, tuner: int) -> dict:
         import torch
         K, d = self.cfg["n_arms"], self.cfg["d"]

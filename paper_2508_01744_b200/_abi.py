@@ -14,7 +14,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("AGFT_LIB_PATH") or os.path.join(HERE, "libagft.so")   # override: A/B builds
 
-ABI_VERSION = 5
+ABI_VERSION = 6
 RECORD_BYTES = 128
 ROW_WORDS = 12
 NO_RECORD = 0xFFFFFFFF
@@ -109,6 +109,7 @@ PROTOTYPES = {
     "agft_stats": (C.c_int, [vp, vp]),
     "agft_export_arms": (C.c_int, [vp, u32, vp, vp, vp, vp, vp, vp, vp]),
     "agft_get_step": (C.c_int, [vp, C.POINTER(u32)]),
+    "agft_get_counters": (C.c_int, [vp, C.POINTER(u32), C.POINTER(u32), C.POINTER(u32)]),
     "agft_run": (C.c_int, [C.POINTER(AgftConfig), vp, vp, u32, u32, vp, C.c_size_t, vp, C.c_size_t,
                            vp, vp, vp]),
     "agft_sweep": (C.c_int, [vp, vp, u32, u32, vp, vp, vp, vp, vp]),

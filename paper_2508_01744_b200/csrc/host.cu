@@ -52,17 +52,6 @@ uint32_t sub_chunk(uint32_t t)
     return late;
 }
 
-// lanes per tuner of the MSEG class (AGFT_MSEG_G ∈ {1, 2, 4, 8}; default 4)
-int mseg_g()
-{
-    static int g = [] {
-        const char *e = std::getenv("AGFT_MSEG_G");
-        const int v = e ? std::atoi(e) : 4;
-        return (v == 1 || v == 2 || v == 4 || v == 8) ? v : 4;
-    }();
-    return g;
-}
-
 bool stream_prio_enabled()
 {
     const char *e = std::getenv("AGFT_STREAM_PRIO");
@@ -87,13 +76,6 @@ void prio_order(int (&rank)[kNumCls])
     }
     for (int c = 0; c < kNumCls; ++c) rank[c] = kNumCls - 1;
     for (int i = kNumCls - 1; i >= 0; --i) rank[order[i]] = i;
-}
-
-// AGFT_LANE_EXACT=1: LANE evaluates the canonical pruning tree every window (tests, A/B)
-uint32_t lane_force_exact()
-{
-    const char *e = std::getenv("AGFT_LANE_EXACT");
-    return (e && e[0] == '1') ? 1u : 0u;
 }
 
 void destroy_streams(agft_handle h)
@@ -133,7 +115,7 @@ agft_status validate(const agft_config *c)
     if (!c) return AGFT_E_INVALID_ARG;
     if (c->abi_version != AGFT_ABI_VERSION) return AGFT_E_INVALID_ARG;
     if (c->n_tuners == 0 || c->n_traces == 0) return AGFT_E_INVALID_ARG;
-    if (c->kernel_policy > AGFT_POLICY_LANE) return AGFT_E_INVALID_ARG;
+    if (c->kernel_policy > AGFT_POLICY_WIDE) return AGFT_E_INVALID_ARG;
     const agft_grid &g = c->grid;
     if (g.n_arms == 0) return AGFT_E_EMPTY_ARMS;
     if (g.f_step_mhz == 0 || g.n_arms > AGFT_MAX_ARMS || g.f_min_mhz == 0) return AGFT_E_INVALID_GRID;
@@ -183,6 +165,52 @@ agft_status validate(const agft_config *c)
     if (!finite(c->prune.cascade_fraction) || c->prune.cascade_fraction <= 0 || c->prune.cascade_fraction > 1)
         return AGFT_E_NONFINITE;
     return AGFT_OK;
+}
+
+// Per-tuner parameters: every index the kernels derive from them must be in range —
+// trace_id selects a trace's records / raw rows, record_slot a row of d_traj / d_gap — and the
+// sweep values must be finite (α0 ≥ 0, k_h ≥ 0).  Host copy of the array.
+agft_status validate_params(const agft_config *c, const agft_tuner_params *p)
+{
+    for (uint32_t i = 0; i < c->n_tuners; ++i) {
+        const agft_tuner_params &q = p[i];
+        if (q.trace_id >= c->n_traces) return AGFT_E_INVALID_ARG;
+        if (q.record_slot != AGFT_NO_RECORD && q.record_slot >= c->record_slots) return AGFT_E_INVALID_ARG;
+        if (!finite(q.alpha0) || q.alpha0 < 0 || !finite(q.extreme_reward_threshold) || !finite(q.historical_k) ||
+            q.historical_k < 0)
+            return AGFT_E_INVALID_ARG;
+    }
+    return AGFT_OK;
+}
+
+// the workspace must live on the current device (kernels and side streams are created there)
+agft_status check_device_ptr(const void *d_ptr, int dev)
+{
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, d_ptr) != cudaSuccess) {
+        cudaGetLastError();
+        return AGFT_E_INVALID_ARG;
+    }
+    if (at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged) return AGFT_E_INVALID_ARG;
+    if (at.type == cudaMemoryTypeDevice && at.device != dev) return AGFT_E_DEVICE;
+    return AGFT_OK;
+}
+
+// copy a device array of n agft_tuner_params to the host and validate it
+agft_status validate_device_params(const agft_config *c, const agft_tuner_params *d_params, cudaStream_t s)
+{
+    agft_tuner_params *hp = static_cast<agft_tuner_params *>(std::malloc(sizeof(agft_tuner_params) * c->n_tuners));
+    if (!hp) return AGFT_E_INVALID_ARG;
+    agft_status st = AGFT_OK;
+    if (cudaMemcpyAsync(hp, d_params, sizeof(agft_tuner_params) * c->n_tuners, cudaMemcpyDeviceToHost, s) !=
+            cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess) {
+        cudaGetLastError();
+        st = AGFT_E_CUDA;
+    }
+    if (st == AGFT_OK) st = validate_params(c, hp);
+    std::free(hp);
+    return st;
 }
 
 agft_status cuda_status(agft_handle h, cudaError_t e)
@@ -283,6 +311,9 @@ agft_status agft_create(const agft_config *cfg, const agft_tuner_params *d_param
     if (cudaGetDevice(&dev) != cudaSuccess) return AGFT_E_DEVICE;
     if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess) return AGFT_E_DEVICE;
     if (major != 10) return AGFT_E_DEVICE;
+    if ((st = check_device_ptr(d_workspace, dev)) != AGFT_OK) return st;
+    if ((st = check_device_ptr(d_params, dev)) != AGFT_OK) return st;
+    if ((st = validate_device_params(cfg, d_params, static_cast<cudaStream_t>(stream))) != AGFT_OK) return st;
 
     agft_handle h = new (std::nothrow) agft_handle_s;
     if (!h) return AGFT_E_INVALID_ARG;
@@ -330,6 +361,11 @@ agft_status agft_attach(const agft_config *cfg, void *d_workspace, size_t ws_byt
     if (cudaGetDevice(&dev) != cudaSuccess) return AGFT_E_DEVICE;
     if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess) return AGFT_E_DEVICE;
     if (major != 10) return AGFT_E_DEVICE;
+    if ((st = check_device_ptr(d_workspace, dev)) != AGFT_OK) return st;
+    // the tuner parameters come from the restored workspace: validated like agft_create's
+    if ((st = validate_device_params(cfg, make_ws(d_workspace, L).params, static_cast<cudaStream_t>(stream))) !=
+        AGFT_OK)
+        return st;
     agft_handle h = new (std::nothrow) agft_handle_s;
     if (!h) return AGFT_E_INVALID_ARG;
     h->cfg = *cfg;
@@ -397,6 +433,11 @@ static agft_status run_steps(agft_handle h, const void *d_records, uint32_t t0, 
                              double *gap, uint32_t *chosen, const uint32_t *raw = nullptr)
 {
     const agft_config &c = h->cfg;
+    // frozen tuners are not scheduled (or return early): their d_chosen entry reads AGFT_NEVER
+    if (chosen) {
+        const cudaError_t e = cudaMemsetAsync(chosen, 0xFF, sizeof(uint32_t) * c.n_tuners, h->stream);
+        if (e != cudaSuccess) return cuda_status(h, e);
+    }
     for (uint32_t s = 0; s < n;) {
         const uint32_t t = t0 + s;
         uint32_t len = sub_chunk(t);
@@ -425,13 +466,7 @@ static agft_status run_steps(agft_handle h, const void *d_records, uint32_t t0, 
         if (c.kernel_policy == AGFT_POLICY_WIDE || (c.refine.enable && !defer)) {
             e = launch_replay(a, c.d, h->stream);
         } else {
-            // MSEG and LANE implement neither the exploitation phase (ENV.md §4.10) nor the closed
-            // loop (§6): AUTO (SOLO / SEG2 / WIDE) instead
-            const bool ext = c.phase.enable || c.closed.enable || defer;   // (+ deferred refinement)
-            const bool split = c.kernel_policy != AGFT_POLICY_MSEG || ext;
-            const bool lane = c.kernel_policy == AGFT_POLICY_LANE && lane_supported(c.d) && !ext;
-            a.force_exact = lane_force_exact();
-            e = launch_classify(h->ws, c.n_tuners, split, h->stream);
+            e = launch_classify(h->ws, c.n_tuners, h->stream);
             if (e == cudaSuccess) e = cudaEventRecord(h->fork, h->stream);
             for (int k = 0; k < kNumCls && e == cudaSuccess; ++k) {
                 ReplayArgs ak = a;
@@ -441,10 +476,9 @@ static agft_status run_steps(agft_handle h, const void *d_records, uint32_t t0, 
                 if (e != cudaSuccess) break;
                 switch (k) {
                 case kClsWide: e = launch_replay(ak, c.d, h->side[k]); break;
-                case kClsSeg32: e = lane ? launch_lane(ak, c.d, 32, h->side[k])
-                                  : split ? launch_seg2(ak, c.d, 16, h->side[k]) : launch_mseg(ak, c.d, mseg_g(), h->side[k]); break;
-                case kClsSeg16: e = lane ? launch_lane(ak, c.d, 16, h->side[k]) : launch_seg2(ak, c.d, 8, h->side[k]); break;
-                case kClsSeg8: e = lane ? launch_lane(ak, c.d, 8, h->side[k]) : launch_seg2(ak, c.d, 4, h->side[k]); break;
+                case kClsSeg32: e = launch_seg2(ak, c.d, 16, h->side[k]); break;
+                case kClsSeg16: e = launch_seg2(ak, c.d, 8, h->side[k]); break;
+                case kClsSeg8: e = launch_seg2(ak, c.d, 4, h->side[k]); break;
                 case kClsSeg64: e = launch_seg2(ak, c.d, 32, h->side[k]); break;
                 default: e = launch_solo(ak, c.d, h->side[k]); break;
                 }
@@ -567,6 +601,8 @@ agft_status agft_regret(agft_handle h, const double *d_S, const double *d_SP, co
 {
     if (!h || !d_S || !d_SP || !d_NP || !d_O || !d_koff) return AGFT_E_INVALID_ARG;
     if (h->sticky != AGFT_OK) return h->sticky;
+    // the sweep is open-loop (ENV.md §5): regret against it is defined for open-loop tuners only
+    if (h->cfg.closed.enable && d_regret) return AGFT_E_INVALID_ARG;
     return cuda_status(h, launch_regret(h->ws, h->cfg, d_S, d_SP, d_NP, d_O, d_koff, d_regret, h->stream));
 }
 
@@ -574,6 +610,15 @@ agft_status agft_get_step(agft_handle h, uint32_t *t)
 {
     if (!h || !t) return AGFT_E_INVALID_ARG;
     *t = h->t;
+    return AGFT_OK;
+}
+
+agft_status agft_get_counters(agft_handle h, uint32_t *t, uint32_t *sweep_t, uint32_t *live_pending)
+{
+    if (!h) return AGFT_E_INVALID_ARG;
+    if (t) *t = h->t;
+    if (sweep_t) *sweep_t = h->sweep_t;
+    if (live_pending) *live_pending = h->live_pending;
     return AGFT_OK;
 }
 
@@ -585,6 +630,7 @@ agft_status agft_run(const agft_config *cfg, const agft_tuner_params *h_params, 
     if (st != AGFT_OK) return st;
     if (!h_params || !d_params_buf || !d_scratch || !d_stats_buf || !h_stats || chunk_steps == 0)
         return AGFT_E_INVALID_ARG;
+    if ((st = validate_params(cfg, h_params)) != AGFT_OK) return st;
     const size_t rec_bytes = (size_t)cfg->n_traces * chunk_steps * AGFT_RECORD_BYTES;
     const size_t raw_bytes = cfg->closed.enable ? (size_t)cfg->n_traces * chunk_steps * AGFT_ROW_WORDS * 4 : 0;
     if (scratch_bytes < rec_bytes + raw_bytes) return AGFT_E_WORKSPACE;

@@ -39,16 +39,6 @@ def test_closed_loop_parity(kw, T, chunk, policy):
     tb.close()
 
 
-@pytest.mark.parametrize("policy", [2, 3])
-def test_closed_loop_falls_back_from_mseg_and_lane(policy):
-    """MSEG and LANE do not implement ENV-C: those policies run the AUTO classes instead."""
-    cfg = with_overrides(named_config("C2"), cl_enable=1, pattern_mode=2, n_tuners=4, n_traces=4)
-    ids = list(range(4))
-    tb, params, st, traj, _ = _run(cfg, 1500, record=ids, chunk=500, policy=policy)
-    _check(cfg, tb, params, st, ids, 1500, traj)
-    tb.close()
-
-
 def test_closed_loop_c4_sampled():
     """One C4 trace's 256 hyper-parameter points under ENV-C for 9,000 windows in the bench's
     launch configuration (all classes, SOLO included); a sample checked against the oracle."""

@@ -90,7 +90,7 @@ def test_c1_parity():
     _check(cfg, tb, params, st, [0], 1000, traj)
 
 
-@pytest.mark.parametrize("policy", [0, 1, 2, 3])
+@pytest.mark.parametrize("policy", [0, 1])
 def test_c2_parity(policy):
     cfg = _cfg("C2")
     tb, params, st, traj, _ = _run(cfg, 4500, record=[0], policy=policy)
@@ -99,7 +99,7 @@ def test_c2_parity(policy):
 
 
 # ---------------------------------------------------------------- batches
-@pytest.mark.parametrize("policy", [0, 1, 2, 3])
+@pytest.mark.parametrize("policy", [0, 1])
 def test_c3_sampled_parity(policy):
     cfg = _cfg("C3")
     sample = [0, 1, 31, 32, 33, 1000, 2047, 4094, 4095]
@@ -133,7 +133,7 @@ def test_c4_full_size_sampled_parity():
     dict(ext_round_limit=1000, ext_min_samples=1),    # extreme pruning + cascades
     dict(f_min_mhz=1200, n_arms=41),                  # no cascade region
 ])
-@pytest.mark.parametrize("policy", [0, 1, 2, 3])
+@pytest.mark.parametrize("policy", [0, 1])
 def test_edge_configs(kw, policy):
     cfg = _cfg("C2", n_tuners=5, n_traces=5, T=700)
     cfg.update(kw)
@@ -204,12 +204,11 @@ def test_invariants_on_gpu_state():
             assert (m[k // 32] >> (k % 32)) & 1
 
 
-@pytest.mark.parametrize("policy", [0, 2, 3])
-def test_scheduled_kernels_agree_with_wide_at_scale(policy):
+def test_scheduled_kernels_agree_with_wide_at_scale():
     """All 4,096 C3 tuners: the class-scheduled kernels (WIDE → SEG → SOLO as arms are pruned)
     reproduce the one-warp-per-tuner schedule bit for bit wherever neither flagged a near-tie."""
     cfg = _cfg("C3")
-    _, _, sa, _, _ = _run(cfg, 4500, policy=policy)
+    _, _, sa, _, _ = _run(cfg, 4500, policy=0)
     _, _, sw, _, _ = _run(cfg, 4500, policy=1)
     ok = (sa["near_tie_steps"] == 0) & (sw["near_tie_steps"] == 0)
     assert ok.mean() > 0.9
@@ -219,37 +218,6 @@ def test_scheduled_kernels_agree_with_wide_at_scale(policy):
     assert np.all(sa["steps"] == 4500) and np.all(sa["n_active"] >= 1)
     # the schedule really exercised the narrow classes
     assert (sa["n_active"] == 1).mean() > 0.5
-
-
-@pytest.mark.parametrize("kw", [
-    dict(),
-    dict(hist_min_round=0, hist_min_samples=1),       # aggressive historical pruning
-    dict(ext_round_limit=1000, ext_min_samples=1),    # extreme pruning + cascades
-    dict(n_arms=20, d=4),                             # LANE at d = 4
-])
-def test_lane_exact_pruning_tree(kw, monkeypatch):
-    """LANE with AGFT_LANE_EXACT=1 evaluates ENV.md §4.8's canonical tree (the member-slot stack)
-    at every window instead of only when the variance screen cannot exclude a removal."""
-    monkeypatch.setenv("AGFT_LANE_EXACT", "1")
-    cfg = _cfg("C2", n_tuners=6, n_traces=6, T=900)
-    cfg.update(kw)
-    ids = list(range(6))
-    params = tuner_params(cfg, ids)
-    params["alpha0"] = np.array([0.0, 0.3, 1.0, 2.0, 5.0, 0.05])
-    params["hist_k"] = np.array([0.5, 1.0, 2.0, 4.0, 4.0, 4.0])
-    tb, params, st, traj, _ = _run(cfg, 900, params=params, record=ids, chunk=256, policy=3)
-    _check(cfg, tb, params, st, ids, 900, traj)
-
-
-def test_lane_screened_paths_free_running():
-    """64 C4 tuners (one trace, the α × τ_E × k_h corner incl. every k_h = 4 point) on LANE
-    without recording, so the near-tie and pruning screens decide; compared with the oracle
-    free-running (bit-exact trajectories and stats)."""
-    cfg = _cfg("C4")
-    ids = list(range(0, 256, 4))
-    params = tuner_params(cfg, ids)
-    tb, params, st, _, _ = _run(cfg, 3000, params=params, chunk=3000, policy=3)
-    _check(cfg, tb, params, st, list(range(len(ids))), 3000, None, arms=True)
 
 
 def test_c5_rank_shard_sampled_parity():

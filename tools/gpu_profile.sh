@@ -1,0 +1,25 @@
+#!/bin/bash
+# One GPU session: tests, measured FP64 peak, the default bench line, the launch list of one
+# bench step and one `ncu --set full` capture per replay class kernel (a steady-state launch).
+#   gpurun --timeout 3000 -- 'bash tools/gpu_profile.sh <tag> [tests|notests]'
+set -u
+TAG=${1:-run}; TESTS=${2:-tests}
+O=gpurun_out/$TAG; mkdir -p $O
+python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/fp64_peak tools/fp64_peak.cu && ./tools/fp64_peak > $O/fp64_peak.json 2>&1
+if [ "$TESTS" = tests ]; then
+  timeout 1800 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
+  timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
+fi
+timeout 900 python bench.py --steps 5 --warmup 3 > $O/bench.json 2> $O/bench.err
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv \
+  python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > $O/launches_bench.log 2>&1
+python tools/launch_summary.py $O/launches.csv > $O/launches_summary.txt 2>&1
+for K in "seg2_kernel<7, 8>" "seg2_kernel<7, 16>" "seg2_kernel<7, 4>" "seg2_kernel<7, 32>" "solo_kernel<7>" "replay_kernel<7, 4, 0>"; do
+  N=$(echo "$K" | tr -dc 'a-z0-9_')
+  SKIP=15; [ "$N" = replay_kernel740 ] && SKIP=2
+  timeout 600 ncu --set full --import-source on --clock-control none --kernel-name-base demangled -k "regex:$K" \
+    --launch-skip $SKIP --launch-count 1 -o $O/ncu_$N -f \
+    python bench.py --T 18000 --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > $O/ncu_$N.log 2>&1
+done
+ls -la $O

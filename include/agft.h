@@ -225,6 +225,14 @@ agft_status agft_step(agft_handle h, const void *d_records, uint32_t *d_chosen);
 agft_status agft_select(agft_handle h, const uint32_t *d_rows, uint32_t *d_chosen);
 agft_status agft_observe(agft_handle h, const double *d_resp);
 
+/* Read-only prediction ("read-only operations (predict, select_*)"): Eq. 1
+ * at the handle's step t for the contexts of d_rows (as agft_select) — d_scores [n_tuners][K] fp64
+ * = θ_fᵀx_t + α_t·√(x_tᵀA_f⁻¹x_t) for every arm f ∈ F_available (α_t = 0 in Exploitation, Eq. 2),
+ * quiet NaN for pruned arms and for every arm of a frozen tuner; d_chosen [n_tuners] (may be NULL)
+ * = the arg max agft_select would return.  Changes no state and does not open a select; returns
+ * AGFT_E_STATE between a select and its observe. */
+agft_status agft_scores(agft_handle h, const uint32_t *d_rows, double *d_scores, uint32_t *d_chosen);
+
 /* The paper's decision loop (§4.2: the context x_t → Eq. 1 arg max over
  * F_available → execute f_t → reward from the measured EDP → Eqs. 3–5 update of the executed
  * arm; then §4.3 pruning) run for n_steps consecutive windows of every tuner, fused

@@ -92,7 +92,7 @@ class OrcRecord(C.Structure):
                 ("reward", C.POINTER(f64)), ("edp", C.POINTER(f64)), ("energy", C.POINTER(f64)),
                 ("tpot", C.POINTER(f64)), ("ttft", C.POINTER(f64)), ("scores", C.POINTER(f64)),
                 ("x", C.POINTER(f64)), ("n_active", C.POINTER(u32)),
-                ("active_mask", C.POINTER(u32)), ("backlog", C.POINTER(u32))]
+                ("active_mask", C.POINTER(u32)), ("backlog", C.POINTER(u32)), ("gap", C.POINTER(f64))]
 
 
 class OrcInject(C.Structure):
@@ -337,7 +337,7 @@ def run_tuner(cfg: dict, tuner: OrcTuner | None = None, T: int | None = None, fo
                 "reward": np.zeros(T), "edp": np.zeros(T), "energy": np.zeros(T),
                 "tpot": np.zeros(T), "ttft": np.zeros(T), "x": np.zeros((T, d)),
                 "n_active": np.zeros(T, np.uint32), "active_mask": np.zeros((T, 4), np.uint32),
-                "backlog": np.zeros(T, np.uint32)}
+                "backlog": np.zeros(T, np.uint32), "gap": np.zeros(T)}
         if scores:
             recd["scores"] = np.zeros((T, K))
         rec = OrcRecord()

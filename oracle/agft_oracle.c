@@ -591,6 +591,17 @@ int orc_run_tuner_ex(const orc_config *c, const orc_tuner *tu, uint32_t T, const
             if (!ok) st->follow_violations++;
             if (kg < K && S->active[kg]) kstar = kg;                  /* adopt the GPU's choice */
         }
+        if (rec && rec->gap) {        /* §4.5: (s_k* − s_k2) / max(m_k*, m_k2), k2 = best other active arm */
+            int k2 = -1;
+            for (uint32_t k = 0; k < K; ++k)
+                if (S->active[k] && k != kstar && (k2 < 0 || s[k] > s[k2])) k2 = (int)k;
+            if (k2 < 0) {
+                rec->gap[t] = INFINITY;
+            } else {
+                double den = mag[kstar] > mag[k2] ? mag[kstar] : mag[k2];
+                rec->gap[t] = den > 0.0 ? (s[kstar] - s[k2]) / den : 0.0;
+            }
+        }
 
         /* a7: response at the chosen frequency; a8: EDP and reward */
         uint32_t F = c->f_min_mhz + kstar * c->f_step_mhz;

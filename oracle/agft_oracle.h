@@ -99,6 +99,7 @@ typedef struct {                       /* optional per-step record (any pointer 
     uint32_t *n_active;                /* [T] after pruning */
     uint32_t *active_mask;             /* [T][4] after pruning (caller zeroes it) */
     uint32_t *backlog;                 /* [T] ENV-C q carried out of window t (§6) */
+    double *gap;                       /* [T] relative top-2 gap of the executed arm (ENV.md §4.5) */
 } orc_record;
 
 typedef struct {                       /* unit-test / live environment: replaces ENV-T/ENV-R */

@@ -19,7 +19,7 @@ from ._abi import (NO_RECORD, PARAMS_DTYPE, RECORD_BYTES, ROW_WORDS, STATS_DTYPE
                    make_config, make_params)
 
 __all__ = ["agft_workspace_bytes", "agft_create", "agft_reset", "agft_trace_generate", "agft_step", "agft_replay",
-           "agft_select", "agft_observe", "agft_replay_raw", "agft_attach",
+           "agft_select", "agft_observe", "agft_scores", "agft_replay_raw", "agft_attach",
            "agft_stats", "agft_export_arms", "agft_get_step", "agft_get_counters", "agft_run", "agft_sweep",
            "agft_regret",
            "agft_destroy", "SweepSums",
@@ -98,6 +98,10 @@ def agft_select(h, rows, chosen):
 
 def agft_observe(h, resp):
     _abi.check("agft_observe", _abi.lib().agft_observe(h, _p(resp)))
+
+
+def agft_scores(h, rows, scores, chosen=None):
+    _abi.check("agft_scores", _abi.lib().agft_scores(h, _p(rows), _p(scores), _p(chosen)))
 
 
 def agft_replay(h, records, t0, n_steps, traj=None, gap=None):
@@ -291,6 +295,16 @@ class TunerBatch:
             chosen = torch.empty(self.n, dtype=torch.int32, device=self.device)
         agft_select(self.h, rows, chosen)
         return chosen
+
+    @_on_device
+    def scores(self, rows):
+        """Read-only Eq. 1 scores [n][K] (float64, NaN for pruned arms) at the current step for the
+        snapshot rows [n][12] (int32 device tensor), and the arg max per tuner."""
+        import torch
+        out = torch.empty((self.n, self.cfg["n_arms"]), dtype=torch.float64, device=self.device)
+        chosen = torch.empty(self.n, dtype=torch.int32, device=self.device)
+        agft_scores(self.h, rows, out, chosen)
+        return out, chosen
 
     @_on_device
     def observe(self, resp):

@@ -104,6 +104,7 @@ PROTOTYPES = {
     "agft_step": (C.c_int, [vp, vp, vp]),
     "agft_select": (C.c_int, [vp, vp, vp]),
     "agft_observe": (C.c_int, [vp, vp]),
+    "agft_scores": (C.c_int, [vp, vp, vp, vp]),
     "agft_replay": (C.c_int, [vp, vp, u32, u32, vp, vp]),
     "agft_replay_raw": (C.c_int, [vp, vp, vp, u32, u32, vp, vp]),
     "agft_stats": (C.c_int, [vp, vp]),

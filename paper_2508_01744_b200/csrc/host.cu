@@ -550,6 +550,19 @@ agft_status agft_select(agft_handle h, const uint32_t *d_rows, uint32_t *d_chose
     return st;
 }
 
+agft_status agft_scores(agft_handle h, const uint32_t *d_rows, double *d_scores, uint32_t *d_chosen)
+{
+    if (!h || !d_rows || !d_scores) return AGFT_E_INVALID_ARG;
+    if (reinterpret_cast<uintptr_t>(d_rows) % 16 != 0) return AGFT_E_INVALID_ARG;
+    if (h->sticky != AGFT_OK) return h->sticky;
+    if (h->live_pending) return AGFT_E_STATE;        // the pending record belongs to the select
+    ReplayArgs a = replay_args(h, nullptr, h->t, 1);
+    a.live_rows = d_rows;
+    a.chosen = d_chosen;
+    a.scores = d_scores;
+    return cuda_status(h, launch_live(a, h->cfg.d, 1, h->stream));
+}
+
 agft_status agft_observe(agft_handle h, const double *d_resp)
 {
     if (!h || !d_resp) return AGFT_E_INVALID_ARG;

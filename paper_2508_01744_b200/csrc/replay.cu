@@ -117,7 +117,9 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
     const uint64_t tb = a.list ? a.list[widx] : widx;
     agft_tuner_stats st = a.w.acc[tb];
     if (st.flags & 1u) {                              // frozen by an earlier anomaly
-        if (MODE == 1 && lane == 0) a.chosen[tb] = AGFT_NEVER;
+        if (MODE == 1 && lane == 0 && a.chosen) a.chosen[tb] = AGFT_NEVER;
+        if (MODE == 1 && a.scores)
+            for (uint32_t k = lane; k < a.K; k += 32) a.scores[tb * a.K + k] = __longlong_as_double(0x7ff8000000000000ll);
         return;
     }
     __shared__ PhState s_ph[kWarpsPerBlock];          // ENV.md §4.10 detector (lane 0 owns it)
@@ -372,6 +374,13 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
         }
         near = __ballot_sync(kFull, tie) != 0u;
         if constexpr (MODE == 1) {                    // select ends here: nothing changes until observe
+            if (a.scores) {                           // agft_scores: every arm's Eq. 1 score (NaN if pruned)
+#pragma unroll
+                for (int j = 0; j < S; ++j) {
+                    const uint32_t k = 32u * j + lane;
+                    if (k < K) a.scores[tb * K + k] = ((act >> j) & 1u) ? sc[j] : __longlong_as_double(0x7ff8000000000000ll);
+                }
+            }
             if (lane == 0) {
                 LivePend pd;
 #pragma unroll
@@ -379,7 +388,7 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
                 pd.kstar = (uint32_t)kstar;
                 pd.near = near ? 1u : 0u;
                 a.w.live[tb] = pd;
-                a.chosen[tb] = (uint32_t)kstar;
+                if (a.chosen) a.chosen[tb] = (uint32_t)kstar;
             }
             return;
         }

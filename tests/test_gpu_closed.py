@@ -34,8 +34,8 @@ def test_closed_loop_parity(kw, T, chunk, policy):
     ids = list(range(6))
     params = tuner_params(cfg, ids)
     params["alpha0"] = np.array([0.0, 0.2, 0.5, 1.0, 2.0, 4.0])
-    tb, params, st, traj, _ = _run(cfg, T, params=params, record=ids, chunk=chunk, policy=policy)
-    _check(cfg, tb, params, st, ids, T, traj)
+    tb, params, st, traj, gap = _run(cfg, T, params=params, record=ids, chunk=chunk, policy=policy)
+    _check(cfg, tb, params, st, ids, T, traj, gap=gap)
     tb.close()
 
 
@@ -46,8 +46,8 @@ def test_closed_loop_c4_sampled():
     ids = list(range(256))
     params = tuner_params(cfg, ids)
     sample = [0, 15, 48, 63, 100, 200, 255]
-    tb, params, st, traj, _ = _run(cfg, 9000, params=params, record=sample, chunk=4500)
-    _check(cfg, tb, params, st, sample, 9000, traj, slots={i: s for s, i in enumerate(sample)})
+    tb, params, st, traj, gap = _run(cfg, 9000, params=params, record=sample, chunk=4500)
+    _check(cfg, tb, params, st, sample, 9000, traj, slots={i: s for s, i in enumerate(sample)}, gap=gap)
     tb.close()
 
 

@@ -41,12 +41,13 @@ def _run(cfg, T, ids=None, record=None, chunk=4500, params=None, policy=0):
     return tb, params, st, traj, gap
 
 
-def _check(cfg, tb, params, st, idx, T, traj=None, slots=None, arms=True):
+def _check(cfg, tb, params, st, idx, T, traj=None, slots=None, arms=True, gap=None):
     problems, infos = [], []
     for s, i in enumerate(idx):
         tr = traj[slots[i] if slots else s] if traj is not None else None
+        gp = gap[slots[i] if slots else s] if gap is not None else None
         g = tb.export_arms(i) if arms else None
-        errs, info = compare_tuner(cfg, params, i, st[i], g, T, tr)
+        errs, info = compare_tuner(cfg, params, i, st[i], g, T, tr, gap=gp)
         problems += errs
         infos.append(info)
     assert not problems, "\n".join(problems[:20])
@@ -86,15 +87,15 @@ def test_trace_records_sampled_full_sizes(name, t0, n, traces):
 # ---------------------------------------------------------------- single tuners (C1, C2)
 def test_c1_parity():
     cfg = _cfg("C1")
-    tb, params, st, traj, _ = _run(cfg, 1000, record=[0])
-    _check(cfg, tb, params, st, [0], 1000, traj)
+    tb, params, st, traj, gap = _run(cfg, 1000, record=[0])
+    _check(cfg, tb, params, st, [0], 1000, traj, gap=gap)
 
 
 @pytest.mark.parametrize("policy", [0, 1])
 def test_c2_parity(policy):
     cfg = _cfg("C2")
-    tb, params, st, traj, _ = _run(cfg, 4500, record=[0], policy=policy)
-    _check(cfg, tb, params, st, [0], 4500, traj)
+    tb, params, st, traj, gap = _run(cfg, 4500, record=[0], policy=policy)
+    _check(cfg, tb, params, st, [0], 4500, traj, gap=gap)
     assert st["n_active"][0] < 107                    # pruning really happened
 
 
@@ -103,8 +104,8 @@ def test_c2_parity(policy):
 def test_c3_sampled_parity(policy):
     cfg = _cfg("C3")
     sample = [0, 1, 31, 32, 33, 1000, 2047, 4094, 4095]
-    tb, params, st, traj, _ = _run(cfg, 4500, record=sample, policy=policy)
-    _check(cfg, tb, params, st, sample, 4500, traj)
+    tb, params, st, traj, gap = _run(cfg, 4500, record=sample, policy=policy)
+    _check(cfg, tb, params, st, sample, 4500, traj, gap=gap)
     assert np.all(st["steps"] == 4500) and np.all(st["flags"] == 0)
 
 
@@ -113,8 +114,8 @@ def test_c4_full_size_sampled_parity():
     configuration; sampled tuners span α, τ_E, k_h and both load patterns."""
     cfg = _cfg("C4")
     sample = [0, 15, 255, 256 + 48, 256 * 77 + 200, 65535]
-    tb, params, st, traj, _ = _run(cfg, cfg["T"], record=sample, chunk=4500)
-    _check(cfg, tb, params, st, sample, cfg["T"], traj)
+    tb, params, st, traj, gap = _run(cfg, cfg["T"], record=sample, chunk=4500)
+    _check(cfg, tb, params, st, sample, cfg["T"], traj, gap=gap)
     assert np.all(st["steps"] == cfg["T"]) and np.all(st["flags"] == 0)
     assert np.all(st["n_active"] >= 1)
 
@@ -140,8 +141,8 @@ def test_edge_configs(kw, policy):
     ids = list(range(5))
     params = tuner_params(cfg, ids)
     params["alpha0"] = np.array([0.0, 0.3, 1.0, 2.0, 5.0])
-    tb, params, st, traj, _ = _run(cfg, 700, params=params, record=ids, chunk=256, policy=policy)
-    _check(cfg, tb, params, st, ids, 700, traj)
+    tb, params, st, traj, gap = _run(cfg, 700, params=params, record=ids, chunk=256, policy=policy)
+    _check(cfg, tb, params, st, ids, 700, traj, gap=gap)
 
 
 def test_ragged_tuner_counts_and_shared_trace():
@@ -150,8 +151,8 @@ def test_ragged_tuner_counts_and_shared_trace():
         cfg = _cfg("C2", n_tuners=n, n_traces=1, T=300)
         params = tuner_params(cfg)
         params["alpha0"] = np.linspace(0.0, 3.0, n)
-        tb, params, st, traj, _ = _run(cfg, 300, params=params, record=list(range(n)))
-        _check(cfg, tb, params, st, list(range(n)), 300, traj, arms=(n <= 3))
+        tb, params, st, traj, gap = _run(cfg, 300, params=params, record=list(range(n)))
+        _check(cfg, tb, params, st, list(range(n)), 300, traj, arms=(n <= 3), gap=gap)
 
 
 def test_step_replay_and_chunking_agree():
@@ -191,7 +192,7 @@ def test_state_error_on_wrong_t0():
 def test_invariants_on_gpu_state():
     """A⁻¹ symmetric (packed) and SPD with eigenvalues in (0, 1]; pruned arms never chosen."""
     cfg = _cfg("C2", n_tuners=8, n_traces=8)
-    tb, params, st, traj, _ = _run(cfg, 1500, record=list(range(8)))
+    tb, params, st, traj, gap = _run(cfg, 1500, record=list(range(8)))
     for i in range(8):
         g = tb.export_arms(i)
         ev = np.linalg.eigvalsh(g["Ainv"])

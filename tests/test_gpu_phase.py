@@ -28,8 +28,8 @@ def _cfg(name, **kw):
 @pytest.mark.parametrize("policy", [0, 1])
 def test_c2_phase_parity(policy):
     cfg = _cfg("C2")
-    tb, params, st, traj, _ = _run(cfg, 4500, record=[0], policy=policy)
-    _check(cfg, tb, params, st, [0], 4500, traj)
+    tb, params, st, traj, gap = _run(cfg, 4500, record=[0], policy=policy)
+    _check(cfg, tb, params, st, [0], 4500, traj, gap=gap)
     assert st["first_exploit_t"][0] != 0xFFFFFFFF and st["exploit_steps"][0] > 0
 
 
@@ -47,8 +47,8 @@ def test_phase_edge_configs(kw, policy):
     ids = list(range(5))
     params = tuner_params(cfg, ids)
     params["alpha0"] = np.array([0.0, 0.3, 1.0, 2.0, 5.0])
-    tb, params, st, traj, _ = _run(cfg, 900, params=params, record=ids, chunk=256, policy=policy)
-    _check(cfg, tb, params, st, ids, 900, traj)
+    tb, params, st, traj, gap = _run(cfg, 900, params=params, record=ids, chunk=256, policy=policy)
+    _check(cfg, tb, params, st, ids, 900, traj, gap=gap)
 
 
 def test_c4_sweep_with_phase_sampled():
@@ -58,8 +58,8 @@ def test_c4_sweep_with_phase_sampled():
     ids = list(range(256))
     params = tuner_params(cfg, ids)
     sample = [0, 15, 48, 63, 100, 200, 255]
-    tb, params, st, traj, _ = _run(cfg, 20000, params=params, record=sample, chunk=4500)
-    _check(cfg, tb, params, st, sample, 20000, traj)
+    tb, params, st, traj, gap = _run(cfg, 20000, params=params, record=sample, chunk=4500)
+    _check(cfg, tb, params, st, sample, 20000, traj, gap=gap)
     assert np.all(st["steps"] == 20000) and np.all(st["flags"] == 0)
     assert (st["exploit_steps"] > 0).mean() > 0.5
 
@@ -81,8 +81,8 @@ def test_refinement_parity(kw, policy):
     ids = list(range(5))
     params = tuner_params(cfg, ids)
     params["alpha0"] = np.array([0.0, 0.3, 1.0, 2.0, 5.0])
-    tb, params, st, traj, _ = _run(cfg, 1500, params=params, record=ids, chunk=512, policy=policy)
-    _check(cfg, tb, params, st, ids, 1500, traj)
+    tb, params, st, traj, gap = _run(cfg, 1500, params=params, record=ids, chunk=512, policy=policy)
+    _check(cfg, tb, params, st, ids, 1500, traj, gap=gap)
     assert np.all(st["n_refine"] > 0)
 
 
@@ -94,8 +94,8 @@ def test_refinement_c4_sample_class_schedule():
     ids = list(range(256))
     params = tuner_params(cfg, ids)
     sample = [0, 5, 31, 64, 130, 200, 255]
-    tb, params, st, traj, _ = _run(cfg, 6000, params=params, record=sample, chunk=4500)
-    _check(cfg, tb, params, st, sample, 6000, traj)
+    tb, params, st, traj, gap = _run(cfg, 6000, params=params, record=sample, chunk=4500)
+    _check(cfg, tb, params, st, sample, 6000, traj, gap=gap)
 
 
 def test_refinement_c4_sample():
@@ -103,5 +103,5 @@ def test_refinement_c4_sample():
     cfg.update(n_traces=1, rf_enable=1, ph_enable=1)
     ids = list(range(0, 256, 8))
     params = tuner_params(cfg, ids)
-    tb, params, st, traj, _ = _run(cfg, 6000, params=params, record=list(range(len(ids))), chunk=4500)
-    _check(cfg, tb, params, st, list(range(len(ids))), 6000, traj)
+    tb, params, st, traj, gap = _run(cfg, 6000, params=params, record=list(range(len(ids))), chunk=4500)
+    _check(cfg, tb, params, st, list(range(len(ids))), 6000, traj, gap=gap)

@@ -15,10 +15,10 @@ timeout 900 python bench.py --steps 5 --warmup 3 > $O/bench.json 2> $O/bench.err
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv \
   python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > $O/launches_bench.log 2>&1
 python tools/launch_summary.py $O/launches.csv > $O/launches_summary.txt 2>&1
-for K in "seg2_kernel<7, 8>" "seg2_kernel<7, 16>" "seg2_kernel<7, 4>" "seg2_kernel<7, 32>" "solo_kernel<7>" "replay_kernel<7, 4, 0>"; do
-  N=$(echo "$K" | tr -dc 'a-z0-9_')
-  SKIP=15; [ "$N" = replay_kernel740 ] && SKIP=2
-  timeout 600 ncu --set full --import-source on --clock-control none --kernel-name-base demangled -k "regex:$K" \
+for K in "seg2_kernel<(int)7, (int)8>" "seg2_kernel<(int)7, (int)16>" "seg2_kernel<(int)7, (int)4>" "seg2_kernel<(int)7, (int)32>" "solo_kernel<(int)7>" "replay_kernel<(int)7, (int)4, (int)0>"; do
+  N=$(echo "$K" | sed 's/(int)//g' | tr -dc 'a-z0-9_')
+  SKIP=${NCU_SKIP:-15}; [ "$N" = replay_kernel740 ] && SKIP=2
+  timeout 600 ncu --set full --import-source on --clock-control none --kernel-name-base demangled -k "regex:$(echo "$K" | sed 's/[()]/\\&/g')" \
     --launch-skip $SKIP --launch-count 1 -o $O/ncu_$N -f \
     python bench.py --T 18000 --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > $O/ncu_$N.log 2>&1
 done

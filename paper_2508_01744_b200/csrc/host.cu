@@ -52,6 +52,21 @@ uint32_t sub_chunk(uint32_t t)
     return late;
 }
 
+// SEG kernel generation: 3 (restructured chain, default) or 2 (round-1 kernel, A/B)
+int seg_impl()
+{
+    static const int v = [] {
+        const char *e = std::getenv("AGFT_SEG");
+        return (e && e[0] == '2') ? 2 : 3;
+    }();
+    return v;
+}
+
+cudaError_t launch_seg(const ReplayArgs &a, uint32_t D, int G, cudaStream_t s)
+{
+    return seg_impl() == 2 ? launch_seg2(a, D, G, s) : launch_seg3(a, D, G, s);
+}
+
 bool stream_prio_enabled()
 {
     const char *e = std::getenv("AGFT_STREAM_PRIO");
@@ -476,10 +491,10 @@ static agft_status run_steps(agft_handle h, const void *d_records, uint32_t t0, 
                 if (e != cudaSuccess) break;
                 switch (k) {
                 case kClsWide: e = launch_replay(ak, c.d, h->side[k]); break;
-                case kClsSeg32: e = launch_seg2(ak, c.d, 16, h->side[k]); break;
-                case kClsSeg16: e = launch_seg2(ak, c.d, 8, h->side[k]); break;
-                case kClsSeg8: e = launch_seg2(ak, c.d, 4, h->side[k]); break;
-                case kClsSeg64: e = launch_seg2(ak, c.d, 32, h->side[k]); break;
+                case kClsSeg32: e = launch_seg(ak, c.d, 16, h->side[k]); break;
+                case kClsSeg16: e = launch_seg(ak, c.d, 8, h->side[k]); break;
+                case kClsSeg8: e = launch_seg(ak, c.d, 4, h->side[k]); break;
+                case kClsSeg64: e = launch_seg(ak, c.d, 32, h->side[k]); break;
                 default: e = launch_solo(ak, c.d, h->side[k]); break;
                 }
                 if (e == cudaSuccess) e = cudaEventRecord(h->join[k], h->side[k]);

@@ -1,0 +1,106 @@
+// seg_common.cuh — warp-segment helpers of the SEG kernels (G lanes per tuner, 32/G tuners per
+// warp): segment ballots and sums, the segment-distributed sorted EDP window (E = 64/G entries per
+// lane), and the canonical 128-slot reduction tree of ENV.md §4.8 over a per-segment buffer.
+#pragma once
+#include "step_common.cuh"
+
+namespace agft {
+
+template <int G>
+__device__ __forceinline__ uint32_t sbits(bool p, int sg)
+{
+    const uint32_t b = __ballot_sync(kFull, p);
+    return G == 32 ? b : (b >> (sg * G)) & ((1u << G) - 1u);
+}
+template <int G>
+__device__ __forceinline__ int spopc(bool p, int sg) { return __popc(sbits<G>(p, sg)); }
+template <int G>
+__device__ __forceinline__ int sisum(int v)
+{
+#pragma unroll
+    for (int off = G / 2; off > 0; off >>= 1) v += __shfl_xor_sync(kFull, v, off, G);
+    return v;
+}
+
+// sorted window element idx (S[l*E + e] in lane l of the segment)
+// (a binary mux tree on the bits of idx % E: a select chain here was compiled into a dynamically
+// indexed local-memory copy of the window — STL ×E/2 + LDL on the reward's serial chain)
+template <int G, int E>
+__device__ __forceinline__ double wat(const double (&S)[E], uint32_t idx)
+{
+    const uint32_t j = idx % E;
+    double v[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e] = S[e];
+#pragma unroll
+    for (int b = 1; b < E; b <<= 1) {
+        const bool up = (j & (uint32_t)b) != 0u;
+#pragma unroll
+        for (int e = 0; e + b < E; e += 2 * b) v[e] = up ? v[e + b] : v[e];
+    }
+    return __shfl_sync(kFull, v[0], idx / E, G);
+}
+template <int G, int E>
+__device__ __forceinline__ int wless(const double (&S)[E], double v)
+{
+    int c = 0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) c += (S[e] < v) ? 1 : 0;
+    return sisum<G>(c);
+}
+template <int G, int E>
+__device__ __forceinline__ void wremove(double (&S)[E], int po, int l)
+{
+    double nxt = __shfl_down_sync(kFull, S[0], 1, G);
+    if (l == G - 1) nxt = kInf;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const double up = (e + 1 < E) ? S[e + 1 < E ? e + 1 : e] : nxt;
+        S[e] = (l * E + e < po) ? S[e] : up;
+    }
+}
+template <int G, int E>
+__device__ __forceinline__ void winsert(double (&S)[E], double v, int pi, int l)
+{
+    const double prv = __shfl_up_sync(kFull, S[E - 1], 1, G);
+#pragma unroll
+    for (int e = E - 1; e >= 0; --e) {
+        const int i = l * E + e;
+        const double dn = (e > 0) ? S[e > 0 ? e - 1 : 0] : prv;
+        S[e] = (i < pi) ? S[e] : ((i == pi) ? v : dn);
+    }
+}
+
+// per-segment tree buffer: slot k at k + k/SL (one pad per 128/G-slot block, odd stride) so
+// that the lanes' block reads fall in different banks
+template <int G>
+__host__ __device__ constexpr int tree_stride() { return 128 + G + 1; }
+template <int G>
+__device__ __forceinline__ int tslot(int k) { return k + k / (128 / G); }
+
+// canonical tree: scatter (has0,key0,v0), (has1,key1,v1) of every lane to `buf`, reduce aligned
+// blocks pairwise, butterfly.  Slots outside the scattered set must hold +0.0: the caller scatters
+// the same set Q (active arms with n ≥ hist_n) in both trees of a step, Q only grows between steps
+// except by pruning, and a pruned arm's slot is zeroed when it is removed (no restore pass here)
+template <int G>
+__device__ __forceinline__ double stree(double *buf, int l, bool h0, int k0, double v0, bool h1, int k1, double v1)
+{
+    constexpr int SL = 128 / G;
+    if (h0) buf[tslot<G>(k0)] = v0;
+    if (h1) buf[tslot<G>(k1)] = v1;
+    __syncwarp();
+    double v[SL];
+#pragma unroll
+    for (int j = 0; j < SL; ++j) v[j] = buf[l * (SL + 1) + j];
+#pragma unroll
+    for (int len = SL; len > 1; len >>= 1)
+#pragma unroll
+        for (int j = 0; j < len / 2; ++j) v[j] = xadd(v[2 * j], v[2 * j + 1]);
+    double s = v[0];
+#pragma unroll
+    for (int off = 1; off < G; off <<= 1) s = xadd(s, __shfl_xor_sync(kFull, s, off, G));
+    __syncwarp();                                     // reads done before the next scatter / zeroing
+    return s;
+}
+
+}  // namespace agft

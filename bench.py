@@ -5,8 +5,9 @@ Workload (one "step" = one pass of the whole hot path, SURVEY §8 rows a0–a11)
 BASELINE configs[3] = C4 — 65,536 tuners per GPU (16 α0 × 16 pruning settings × 256
 traces, diurnal + burst load), the full 107-arm grid, d = 7, 24 h = 108,000 decision
 windows.  Per step: reset tuners → [trace records (K1) → replay (K2)] × 24 chunks →
-stats (→ NCCL all-gather of stats when N > 1).  Weak scaling: every rank runs its own
-C4 shard (traces offset by rank), so total work grows with N.
+stats (→ NCCL all-gather of stats and a 16×u64 counter all-reduce when N > 1).  Strong
+scaling: the 65,536 tuners and their 256 traces are split over the N ranks
+(65,536/N tuners per GPU, whole traces per rank, no input exchange).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
   torchrun --nproc-per-node N bench.py --gpus N ...
@@ -35,46 +36,49 @@ UNIT = "tuner-steps/s"
 CHUNK = 4500                     # decision windows per replay launch (1 h of trace)
 FP64_UNITS_PER_SM = 64           # FP64 FMA lanes per SM (B200)
 N_SM = 148
+STATS_DTYPE_BYTES = 128
 
 
-def profile_traffic():
-    """DRAM bytes (read + write) of all replay-class launches of one default bench step, from
-    the committed ncu capture (tools/gpu_traffic.sh → profiles/r01_v13_traffic.json), or None."""
-    path = os.path.join(ROOT, "profiles", "r01_v13_traffic.json")
-    try:
-        with open(path) as f:
-            tot = json.load(f)["_replay_total"]
-        return tot["dram_bytes"], ("ncu dram__bytes_read+write summed over the replay launches of one "
-                                   "C4 bench step (profiles/r01_v13_traffic.json)")
-    except (OSError, KeyError, ValueError):
-        return None, None
+def src_sha() -> str:
+    """Hash of the CUDA sources and the ABI header: ties an ncu capture to the build it measured."""
+    import hashlib
+    h = hashlib.sha256()
+    for d in (os.path.join(ROOT, "paper_2508_01744_b200", "csrc"), os.path.join(ROOT, "include")):
+        for name in sorted(os.listdir(d)):
+            if name.endswith((".cu", ".cuh", ".h")):
+                with open(os.path.join(d, name), "rb") as f:
+                    h.update(name.encode() + b"\0" + f.read())
+    return h.hexdigest()[:16]
 
 
-def profile_utilisation():
-    """The three ncu utilisations SURVEY §8(d) asks for, of the dominant replay kernel, from the
-    committed ncu --set full capture (profiles/r01_v13_ncu_full_seg8.txt), or None."""
-    path = os.path.join(ROOT, "profiles", "r01_v13_ncu_full_seg8.txt")
-    keys = {"sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active": "fp64_pipe_pct",
-            "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed": "smem_pct",
-            "smsp__issue_active.avg.pct_of_peak_sustained_active": "issue_active_pct",
-            "sm__warps_active.avg.pct_of_peak_sustained_active": "warps_active_pct"}
-    out = {}
-    try:
-        with open(path) as f:
-            lines = f.read().splitlines()
-    except OSError:
-        return None
-    for ln in lines:
-        parts = ln.split()
-        if len(parts) >= 2 and parts[0] in keys:
-            out[keys[parts[0]]] = float(parts[1])
-        if ln.startswith("== "):
-            out["kernel"] = ln[3:].strip()
-        if parts and parts[0] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-            out.setdefault("dram_mbytes", 0.0)
-            out["dram_mbytes"] += float(parts[1])
-    out["source"] = "profiles/r01_v13_ncu_full_seg8.txt (one launch, ncu --set full)"
-    return out
+def profile_traffic(workload_key: str):
+    """ncu DRAM read + write bytes per launch of each replay class, from the capture of one bench step
+    of THIS build and workload (tools/ncu_traffic.py → profiles/*_traffic.json, matched on the source
+    hash and the workload key), or None when no capture of this build exists."""
+    import glob
+    sha = src_sha()
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_traffic.json")), reverse=True):
+        try:
+            with open(path) as f:
+                tr = json.load(f)
+        except (OSError, ValueError):
+            continue
+        if tr.get("src_sha") == sha and tr.get("workload_key") == workload_key:
+            tr["source"] = os.path.relpath(path, ROOT)
+            return tr
+    return None
+
+
+def measured_fp64_peak():
+    """FP64 DFMA TFLOP/s measured on a B200 of this pool by tools/fp64_peak.cu (profiles/*fp64_peak.json)."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*fp64_peak.json")), reverse=True):
+        try:
+            with open(path) as f:
+                return float(json.load(f)["fp64_dfma_tflops"]), os.path.relpath(path, ROOT)
+        except (OSError, ValueError, KeyError):
+            continue
+    return None, None
 
 
 def flops_per_step(d: int, k_act_sum: float, steps: float) -> float:
@@ -203,6 +207,66 @@ def parity_summary(gst, ost) -> dict:
             "oracle": "free-running fp64 C oracle of the cpu_baseline leg, same config and windows"}
 
 
+def workload_key(args, cfg, n, R, T, chunk) -> str:
+    return (f"{args.config}:n={n}:R={R}:T={T}:ph={int(bool(cfg.get('ph_enable')))}:rf={int(bool(cfg.get('rf_enable')))}"
+            f":cl={int(bool(cfg.get('cl_enable')))}:pol={args.policy}:chunk={chunk}")
+
+
+def class_roofline(d, prof, prof_conc, steps, replay_ms, serial_replay_ms, st, n, T, R, traffic) -> dict:
+    """SURVEY §8(d) roofline per replay class (agft_profile_*: tuner-steps and Σ K_act each class's
+    kernels processed, and CUDA-event times of its launches).  ``prof`` is one C4 day with every class
+    kernel alone on the stream (per-kernel durations); ``prof_conc`` the timed region itself, where
+    the classes of a sub-chunk run concurrently on their own streams (a class's event span includes
+    its wait for SMs held by the others).  Algorithmic flops ÷ the kernel's own time,
+    against the FP64 peak; the dominant kernel is the class with the most kernel time."""
+    pk = peaks()
+    sm_mhz = float(pk.get("sm_max_mhz", 1965.0))
+    peak_fp64 = N_SM * FP64_UNITS_PER_SM * 2 * sm_mhz * 1e6 / 1e12
+    meas, meas_src = measured_fp64_peak()
+    classes = {}
+    for name, c in prof.items():
+        if not c["launches"]:
+            continue
+        e = {"launches": c["launches"], "kernel_ms": round(c["kernel_ms"], 3),
+             "ms_per_launch": round(c["kernel_ms"] / c["launches"], 4)}
+        if c["tuner_steps"]:
+            fl = flops_per_step(d, float(c["active_arm_steps"]), float(c["tuner_steps"]))
+            ach = fl / (c["kernel_ms"] / 1e3) / 1e12
+            e.update({"share_of_serial_step": round(c["kernel_ms"] / serial_replay_ms, 4),
+                      "concurrent_span_ms_per_step": round(prof_conc[name]["kernel_ms"] / steps, 3),
+                      "tuner_steps": c["tuner_steps"], "mean_active_arms": round(c["active_arm_steps"] / c["tuner_steps"], 3),
+                      "tuner_steps_per_s": round(c["tuner_steps"] / (c["kernel_ms"] / 1e3), 1),
+                      "achieved_tflops": round(ach, 4), "frac": round(ach / peak_fp64, 5)})
+        if traffic and name in traffic.get("classes", {}):
+            tc = traffic["classes"][name]
+            e["traffic_per_launch"] = tc["dram_bytes"] / max(1, tc["launches"])
+        classes[name] = e
+    replay = {k: v for k, v in classes.items() if "tuner_steps" in v}
+    top = max(replay, key=lambda k: replay[k]["kernel_ms"]) if replay else None
+    sum_active = float(np.sum(st["sum_active"], dtype=np.float64))
+    step_flops = flops_per_step(d, sum_active, float(n) * T) * steps
+    out = {"bound": "alu", "kernel": top, "unit": "TFLOP/s",
+           "peak": round(peak_fp64, 2),
+           "peak_source": "derived: 148 SM × 64 FP64 FMA/clk × 2 × sm_max_mhz (DESIGN.md §5)",
+           "peak_measured": meas, "peak_measured_source": meas_src}
+    if top:
+        t = replay[top]
+        out.update({"achieved": t["achieved_tflops"], "frac": t["frac"],
+                    "frac_of_measured_peak": round(t["achieved_tflops"] / meas, 5) if meas else None,
+                    "traffic": t.get("traffic_per_launch")})
+    out.update({"attribution": "one extra C4 day with each class kernel alone on the stream (agft_profile_start(h, 1)); "
+                               f"serialised replay {serial_replay_ms:.1f} ms vs {replay_ms / steps:.1f} ms concurrent",
+                "whole_replay": {"achieved_tflops": round(step_flops / (replay_ms / 1e3) / 1e12, 4),
+                                 "frac": round(step_flops / (replay_ms / 1e3) / 1e12 / peak_fp64, 5),
+                                 "replay_ms": round(replay_ms, 3), "mean_active_arms": round(sum_active / (float(n) * T), 3)},
+                "classes": classes,
+                "traffic_source": traffic.get("source") if traffic else None,
+                "traffic_total_bytes_per_step": traffic.get("total_dram_bytes") if traffic else None,
+                # records once (128 B per window and trace) + the stats (DESIGN.md §5)
+                "algorithmic_hbm_bytes_per_step": 128 * T * R + STATS_DTYPE_BYTES * n})
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -223,15 +287,16 @@ def main():
     ap.add_argument("--policy", type=int, default=int(os.environ.get("AGFT_POLICY", "0")),
                     help="0 auto (SOLO/SEG/WIDE), 1 wide only, 2 SOLO/MSEG/WIDE")
     ap.add_argument("--scaling", default=None, choices=["weak", "strong"],
-                    help="weak: every rank runs the full config (default for C1-C4); strong: split it (C5)")
+                    help="strong: split the config's tuners over the ranks (default for C4, C5); weak: every rank "
+                         "runs the full config (default for C1-C3)")
     ap.add_argument("--backend", default="nccl", help="process-group backend for N > 1 (nccl; gloo for tests)")
     ap.add_argument("--workload", default="replay", choices=["replay", "sweep", "live"],
                     help="replay: the tuner hot path (north-star metric); sweep: ENV.md §5 offline sweep; "
                          "live: agft_select/agft_observe decision latency")
     ap.add_argument("--tuners", type=int, default=1024, help="live workload: tuners per GPU")
     args = ap.parse_args()
-    if args.scaling is None:
-        args.scaling = "strong" if args.config == "C5" else "weak"
+    if args.scaling is None:                 # C4 and C5 split their tuners over the ranks
+        args.scaling = "strong" if args.config in ("C4", "C5") else "weak"
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -321,6 +386,7 @@ def main():
         dist.barrier()
     from paper_2508_01744_b200 import _abi
     launches0 = _abi.lib().agft_kernel_launches()
+    pkg.agft_profile_start(tb.h)
     start.record(stream)
     for _ in range(args.steps):
         one_step(True)
@@ -330,8 +396,17 @@ def main():
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
+    prof_conc = pkg.agft_profile_read(tb.h)
     ms = start.elapsed_time(end)
     replay_ms = sum(a.elapsed_time(b) for a, b in ev_replay)
+    # per-kernel attribution: one more step, untimed for the headline, with every class
+    # kernel alone on the stream so that each CUDA-event pair times exactly one kernel
+    pkg.agft_profile_start(tb.h, serialize=True)
+    ev_replay.clear()
+    one_step(True)
+    torch.cuda.synchronize()
+    prof = pkg.agft_profile_read(tb.h)
+    serial_replay_ms = sum(a.elapsed_time(b) for a, b in ev_replay)
     if world > 1:
         t_ = torch.tensor([ms], dtype=torch.float64, device=coll_dev)
         dist.all_reduce(t_, op=dist.ReduceOp.MAX)
@@ -341,24 +416,13 @@ def main():
     steps_ok = bool(np.all(st["steps"] == T)) and bool(np.all(st["flags"] == 0))
     units = float(n) * T * world * args.steps
     value = units / (ms / 1e3)
+    # one 16×u64 counter all-reduce (steps, flags, near-ties, invariant violations)
+    counters = shard.reduce_counters(shard.counter_vector(st, T), coll_dev) if world > 1 else \
+        dict(zip(shard.COUNTER_NAMES, shard.counter_vector(st, T)))
 
-    # roofline of the dominant kernel (replay): algorithmic FP64 flops / its event time
-    sum_active = float(np.sum(st["sum_active"], dtype=np.float64))
-    flops_rank_step = flops_per_step(cfg["d"], sum_active, float(n) * T)
-    achieved = flops_rank_step * args.steps / (replay_ms / 1e3) / 1e12
-    pk = peaks()
-    sm_mhz = float(pk.get("sm_max_mhz", 1965.0))
-    peak_fp64 = N_SM * FP64_UNITS_PER_SM * 2 * sm_mhz * 1e6 / 1e12
-    traffic, traffic_src = profile_traffic()
-    roofline = {"bound": "alu", "achieved": round(achieved, 4), "peak": round(peak_fp64, 2),
-                "unit": "TFLOP/s", "frac": round(achieved / peak_fp64, 5), "traffic": traffic,
-                "traffic_scope": traffic_src,
-                "algorithmic_hbm_bytes_per_step": 128 * T * R + STATS_DTYPE.itemsize * n,   # records once + stats
-                "kernel": "replay_kernel", "replay_share": round(replay_ms / ms, 4),
-                "peak_source": "derived: 148 SM × 64 FP64 FMA/clk × 2 × sm_max_mhz (DESIGN.md §5)",
-                "mean_active_arms": round(sum_active / (float(n) * T), 3),
-                "ncu_top_kernel": profile_utilisation()}
-
+    wkey = workload_key(args, cfg, n, R, T, chunk)
+    roofline = class_roofline(cfg["d"], prof, prof_conc, args.steps, replay_ms, serial_replay_ms, st, n, T, R,
+                              profile_traffic(wkey))
     out = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -373,7 +437,7 @@ def main():
                       "l2": f"inputs larger than L2: tuner state {tb.workspace.numel() / 2**30:.2f} GiB/GPU",
                       "parallelism": f"tuner shards dp{world}"},
            "roofline": roofline, "clocks": clk,
-           "gpu_launches": launches, "all_steps_complete": steps_ok}
+           "gpu_launches": launches, "all_steps_complete": steps_ok, "counters": counters}
 
     if not args.no_e2e:
         out["e2e"] = e2e_leg(cfg, params, sh.trace_base, world, local, chunk, n, T, args)

@@ -30,8 +30,9 @@
 extern "C" {
 #endif
 
-#define AGFT_ABI_VERSION 6u         /* 2: + agft_phase; 3: + agft_refine (and their stats); 4: + agft_select/agft_observe;
-                                       5: + agft_closed / agft_replay_raw; 6: MSEG/LANE policies retired */
+#define AGFT_ABI_VERSION 7u         /* 2: + agft_phase; 3: + agft_refine (and their stats); 4: + agft_select/agft_observe;
+                                       5: + agft_closed / agft_replay_raw; 6: MSEG/LANE policies retired;
+                                       7: + agft_profile_start / agft_profile_read (workspace +128 B) */
 #define AGFT_MAX_ARMS 128u          /* K ≤ 128 */
 #define AGFT_MAX_D 7u               /* the paper's 7-dim context */
 #define AGFT_MAX_WINDOW 64u         /* reward-median window, AMB-3 */
@@ -309,6 +310,30 @@ agft_status agft_sweep(agft_handle h, const void *d_records, uint32_t t0, uint32
  * The sweep is open-loop (ENV.md §5): d_regret on a closed-loop handle returns AGFT_E_INVALID_ARG. */
 agft_status agft_regret(agft_handle h, const double *d_S, const double *d_SP, const uint32_t *d_NP,
                         const double *d_O, uint8_t *d_koff, double *d_regret);
+
+/* ---- Per-class accounting (measurement; SURVEY §8(d) asks for the roofline of the dominant kernel,
+ * and the replay runs one kernel per active-arm class).  Slots 0..5 are the replay classes
+ * (0 WIDE K_act > 64 or the WIDE schedule, 1 SEG G=16 (17–32 arms), 2 SEG G=8 (9–16), 3 SEG G=4
+ * (2–8), 4 SOLO (1 arm), 5 SEG G=32 (33–64)), 6 the classification kernels, 7 the refinement pass.
+ * agft_profile_start zeroes the counters and records a timed CUDA event pair on the launching
+ * stream around every later launch.  serialize = 0 keeps the product schedule (the classes of a
+ * sub-chunk run concurrently on their own streams, so a class's event time spans its wait for SMs
+ * held by the others); serialize = 1 runs every class alone on the handle's stream, so each event
+ * pair times one kernel (results are identical either way).  agft_profile_read synchronises the
+ * handle's stream and returns:
+ *   tuner_steps[c]      tuner-steps the class's kernels processed (Σ over its tuners of the steps)
+ *   active_arm_steps[c] Σ over those tuner-steps of |F_available| before pruning (the Eq. 1 work)
+ *   kernel_ms[c]        Σ over the class's launches of the event time on its launching stream
+ *   launches[c]         launches recorded
+ * and stops recording.  Profiling adds two events per launch and two atomics per tuner and launch. */
+typedef struct {
+    uint64_t tuner_steps[8];
+    uint64_t active_arm_steps[8];
+    double kernel_ms[8];
+    uint32_t launches[8];
+} agft_profile;
+agft_status agft_profile_start(agft_handle h, int serialize);
+agft_status agft_profile_read(agft_handle h, agft_profile *out);
 
 /* Frees the host handle only; the caller frees its device buffers. */
 agft_status agft_destroy(agft_handle h);

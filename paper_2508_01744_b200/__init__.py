@@ -135,6 +135,20 @@ def agft_get_counters(h) -> tuple[int, int, int]:
     return t.value, sw.value, lp.value
 
 
+def agft_profile_start(h, serialize: bool = False):
+    """Start per-class accounting; serialize=True runs each class alone (per-kernel event times)."""
+    _abi.check("agft_profile_start", _abi.lib().agft_profile_start(h, int(bool(serialize))))
+
+
+def agft_profile_read(h) -> dict:
+    """Per-class tuner-steps, Σ K_act, event time and launches since agft_profile_start (synchronises)."""
+    p = _abi.AgftProfile()
+    _abi.check("agft_profile_read", _abi.lib().agft_profile_read(h, C.byref(p)))
+    return {name: {"tuner_steps": int(p.tuner_steps[i]), "active_arm_steps": int(p.active_arm_steps[i]),
+                   "kernel_ms": float(p.kernel_ms[i]), "launches": int(p.launches[i])}
+            for i, name in enumerate(_abi.PROFILE_SLOTS)}
+
+
 def agft_sweep(h, records, t0, n_steps, S, SP, NP, O, best=None):
     _abi.check("agft_sweep", _abi.lib().agft_sweep(h, _p(records), t0, n_steps, _p(S), _p(SP), _p(NP), _p(O),
                                                     _p(best)))

@@ -14,7 +14,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("AGFT_LIB_PATH") or os.path.join(HERE, "libagft.so")   # override: A/B builds
 
-ABI_VERSION = 6
+ABI_VERSION = 7
 RECORD_BYTES = 128
 ROW_WORDS = 12
 NO_RECORD = 0xFFFFFFFF
@@ -118,7 +118,17 @@ PROTOTYPES = {
     "agft_destroy": (C.c_int, [vp]),
     "agft_status_string": (C.c_char_p, [C.c_int]),
     "agft_kernel_launches": (C.c_uint64, []),
+    "agft_profile_start": (C.c_int, [vp, C.c_int]),
+    "agft_profile_read": (C.c_int, [vp, vp]),
 }
+
+# agft_profile slots (include/agft.h): the replay classes, then the classification and refinement passes
+PROFILE_SLOTS = ("wide", "seg_g16", "seg_g8", "seg_g4", "solo", "seg_g32", "classify", "refine")
+
+
+class AgftProfile(C.Structure):
+    _fields_ = [("tuner_steps", u64 * 8), ("active_arm_steps", u64 * 8), ("kernel_ms", f64 * 8),
+                ("launches", u32 * 8)]
 
 _lib = None
 

@@ -9,7 +9,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libagft.so")
-SOURCES = ["host.cu", "trace.cu", "replay.cu", "replay_seg2.cu", "replay_seg3.cu", "replay_solo.cu", "schedule.cu", "sweep.cu"]
+SOURCES = ["host.cu", "trace.cu", "replay.cu", "replay_seg2.cu", "replay_solo.cu", "schedule.cu", "sweep.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off"]

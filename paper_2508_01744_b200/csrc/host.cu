@@ -6,6 +6,7 @@
 #include <cstring>
 #include <atomic>
 #include <new>
+#include <vector>
 
 #include "agft_internal.cuh"
 
@@ -22,6 +23,14 @@ struct agft_handle_s {
     uint32_t sweep_t;       // next window of the offline sweep (ENV.md §5 accumulation order)
     uint32_t live_pending;  // 1 between agft_select and its agft_observe
     agft_status sticky;     // AGFT_OK or AGFT_E_CUDA
+    // agft_profile_*: per-class launch events (timed, on the class's stream) while profiling is on
+    struct ProfEv {
+        int cls;
+        cudaEvent_t a, b;
+    };
+    bool prof_on, prof_serial;
+    std::vector<ProfEv> prof_ev;
+    size_t prof_used;
 };
 
 namespace agft {
@@ -52,20 +61,7 @@ uint32_t sub_chunk(uint32_t t)
     return late;
 }
 
-// SEG kernel generation: 3 (restructured chain, default) or 2 (round-1 kernel, A/B)
-int seg_impl()
-{
-    static const int v = [] {
-        const char *e = std::getenv("AGFT_SEG");
-        return (e && e[0] == '2') ? 2 : 3;
-    }();
-    return v;
-}
-
-cudaError_t launch_seg(const ReplayArgs &a, uint32_t D, int G, cudaStream_t s)
-{
-    return seg_impl() == 2 ? launch_seg2(a, D, G, s) : launch_seg3(a, D, G, s);
-}
+cudaError_t launch_seg(const ReplayArgs &a, uint32_t D, int G, cudaStream_t s) { return launch_seg2(a, D, G, s); }
 
 bool stream_prio_enabled()
 {
@@ -340,6 +336,9 @@ agft_status agft_create(const agft_config *cfg, const agft_tuner_params *d_param
     h->sweep_t = 0;
     h->live_pending = 0;
     h->sticky = AGFT_OK;
+    h->prof_on = false;
+    h->prof_serial = false;
+    h->prof_used = 0;
     h->fork = nullptr;
     for (int c = 0; c < kNumCls; ++c) {
         h->side[c] = nullptr;
@@ -391,6 +390,9 @@ agft_status agft_attach(const agft_config *cfg, void *d_workspace, size_t ws_byt
     h->sweep_t = sweep_t;
     h->live_pending = 0;
     h->sticky = AGFT_OK;
+    h->prof_on = false;
+    h->prof_serial = false;
+    h->prof_used = 0;
     h->fork = nullptr;
     for (int c = 0; c < kNumCls; ++c) {
         h->side[c] = nullptr;
@@ -442,6 +444,32 @@ agft_status agft_trace_generate(agft_handle h, uint32_t t0, uint32_t n_steps, vo
     return cuda_status(h, launch_trace(a, h->stream));
 }
 
+constexpr int kProfClassify = 6, kProfRefine = 7;   // agft_profile slots after the kernel classes
+
+// agft_profile_*: a timed event pair around one launch of class cls on stream st (no-op when off)
+static cudaError_t prof_begin(agft_handle h, int cls, cudaStream_t st, ReplayArgs *a)
+{
+    if (!h->prof_on) return cudaSuccess;
+    if (a) {
+        a->prof = h->ws.prof;
+        a->prof_cls = (uint32_t)cls;
+    }
+    if (h->prof_used == h->prof_ev.size()) {
+        agft_handle_s::ProfEv ev{cls, nullptr, nullptr};
+        cudaError_t e = cudaEventCreate(&ev.a);
+        if (e == cudaSuccess) e = cudaEventCreate(&ev.b);
+        if (e != cudaSuccess) return e;
+        h->prof_ev.push_back(ev);
+    }
+    h->prof_ev[h->prof_used].cls = cls;
+    return cudaEventRecord(h->prof_ev[h->prof_used].a, st);
+}
+static cudaError_t prof_end(agft_handle h, cudaStream_t st)
+{
+    if (!h->prof_on) return cudaSuccess;
+    return cudaEventRecord(h->prof_ev[h->prof_used++].b, st);
+}
+
 // The replay scheduler: steps [t0, t0+n) in sub-chunks; before each sub-chunk every tuner
 // is classified by its active-arm count and each class runs its kernel on its own stream.
 static agft_status run_steps(agft_handle h, const void *d_records, uint32_t t0, uint32_t n, uint8_t *traj,
@@ -479,25 +507,34 @@ static agft_status run_steps(agft_handle h, const void *d_records, uint32_t t0, 
         // refinement re-admits arms, so a tuner's class can grow: without the deferred pass, one
         // warp per tuner throughout
         if (c.kernel_policy == AGFT_POLICY_WIDE || (c.refine.enable && !defer)) {
-            e = launch_replay(a, c.d, h->stream);
+            e = prof_begin(h, kClsWide, h->stream, &a);
+            if (e == cudaSuccess) e = launch_replay(a, c.d, h->stream);
+            if (e == cudaSuccess) e = prof_end(h, h->stream);
         } else {
-            e = launch_classify(h->ws, c.n_tuners, h->stream);
+            e = prof_begin(h, kProfClassify, h->stream, nullptr);
+            if (e == cudaSuccess) e = launch_classify(h->ws, c.n_tuners, h->stream);
+            if (e == cudaSuccess) e = prof_end(h, h->stream);
             if (e == cudaSuccess) e = cudaEventRecord(h->fork, h->stream);
             for (int k = 0; k < kNumCls && e == cudaSuccess; ++k) {
                 ReplayArgs ak = a;
                 ak.list = h->ws.lists + (size_t)k * c.n_tuners;
                 ak.count = h->ws.counts + k;
-                e = cudaStreamWaitEvent(h->side[k], h->fork, 0);
+                // agft_profile_start(h, 1): every class alone on the handle's stream (per-kernel times)
+                const cudaStream_t sk = h->prof_on && h->prof_serial ? h->stream : h->side[k];
+                if (sk != h->stream) e = cudaStreamWaitEvent(sk, h->fork, 0);
+                if (e == cudaSuccess) e = prof_begin(h, k, sk, &ak);
                 if (e != cudaSuccess) break;
                 switch (k) {
-                case kClsWide: e = launch_replay(ak, c.d, h->side[k]); break;
-                case kClsSeg32: e = launch_seg(ak, c.d, 16, h->side[k]); break;
-                case kClsSeg16: e = launch_seg(ak, c.d, 8, h->side[k]); break;
-                case kClsSeg8: e = launch_seg(ak, c.d, 4, h->side[k]); break;
-                case kClsSeg64: e = launch_seg(ak, c.d, 32, h->side[k]); break;
-                default: e = launch_solo(ak, c.d, h->side[k]); break;
+                case kClsWide: e = launch_replay(ak, c.d, sk); break;
+                case kClsSeg32: e = launch_seg(ak, c.d, 16, sk); break;
+                case kClsSeg16: e = launch_seg(ak, c.d, 8, sk); break;
+                case kClsSeg8: e = launch_seg(ak, c.d, 4, sk); break;
+                case kClsSeg64: e = launch_seg(ak, c.d, 32, sk); break;
+                default: e = launch_solo(ak, c.d, sk); break;
                 }
-                if (e == cudaSuccess) e = cudaEventRecord(h->join[k], h->side[k]);
+                if (e == cudaSuccess) e = prof_end(h, sk);
+                if (sk == h->stream) continue;
+                if (e == cudaSuccess) e = cudaEventRecord(h->join[k], sk);
                 if (e == cudaSuccess) e = cudaStreamWaitEvent(h->stream, h->join[k], 0);
             }
         }
@@ -505,7 +542,9 @@ static agft_status run_steps(agft_handle h, const void *d_records, uint32_t t0, 
             ReplayArgs r = replay_args(h, d_records, t + len - 1, 1);   // as of the sub-chunk's last step
             r.rec_stride = n;
             r.rec_off = s + len - 1;
-            e = launch_refine(r, c.d, h->stream);
+            e = prof_begin(h, kProfRefine, h->stream, nullptr);
+            if (e == cudaSuccess) e = launch_refine(r, c.d, h->stream);
+            if (e == cudaSuccess) e = prof_end(h, h->stream);
         }
         if (e != cudaSuccess) return cuda_status(h, e);
         s += len;
@@ -693,7 +732,45 @@ agft_status agft_destroy(agft_handle h)
     if (!h) return AGFT_E_INVALID_ARG;
     cudaStreamSynchronize(h->stream);
     destroy_streams(h);
+    for (auto &ev : h->prof_ev) {
+        cudaEventDestroy(ev.a);
+        cudaEventDestroy(ev.b);
+    }
     delete h;
+    return AGFT_OK;
+}
+
+agft_status agft_profile_start(agft_handle h, int serialize)
+{
+    if (!h || serialize < 0 || serialize > 1) return AGFT_E_INVALID_ARG;
+    if (h->sticky != AGFT_OK) return h->sticky;
+    h->prof_on = true;
+    h->prof_serial = serialize != 0;
+    h->prof_used = 0;
+    return cuda_status(h, cudaMemsetAsync(h->ws.prof, 0, 16 * sizeof(unsigned long long), h->stream));
+}
+
+agft_status agft_profile_read(agft_handle h, agft_profile *out)
+{
+    if (!h || !out) return AGFT_E_INVALID_ARG;
+    if (h->sticky != AGFT_OK) return h->sticky;
+    std::memset(out, 0, sizeof(*out));
+    unsigned long long cnt[16];
+    cudaError_t e = cudaMemcpyAsync(cnt, h->ws.prof, sizeof(cnt), cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);   // every class stream joins it
+    for (size_t i = 0; i < h->prof_used && e == cudaSuccess; ++i) {
+        float ms = 0.f;
+        e = cudaEventElapsedTime(&ms, h->prof_ev[i].a, h->prof_ev[i].b);
+        out->kernel_ms[h->prof_ev[i].cls] += ms;
+        out->launches[h->prof_ev[i].cls] += 1u;
+    }
+    if (e != cudaSuccess) return cuda_status(h, e);
+    for (int c = 0; c < 8; ++c) {
+        out->tuner_steps[c] = cnt[c];
+        out->active_arm_steps[c] = cnt[8 + c];
+    }
+    h->prof_on = false;
+    h->prof_used = 0;
     return AGFT_OK;
 }
 

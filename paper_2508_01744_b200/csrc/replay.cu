@@ -677,6 +677,7 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
             a.w.ph[tb] = s_ph[warp];
             ph_to_stats(s_ph[warp], st);
         }
+        prof_add(a, a.w.acc + tb, st);
         a.w.acc[tb] = st;
     }
     if (a.rf_enable) {

@@ -466,6 +466,7 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
             a.w.ph[tb] = ph;
             ph_to_stats(ph, st);
         }
+        prof_add(a, a.w.acc + tb, st);
         a.w.acc[tb] = st;
     }
 }

@@ -153,6 +153,7 @@ __global__ void __launch_bounds__(kSoloThreads, kSoloMinBlocks) solo_kernel(cons
         a.w.ph[tb] = ph;
         ph_to_stats(ph, st);
     }
+    prof_add(a, a.w.acc + tb, st);
     a.w.acc[tb] = st;
 #undef SW
 }

@@ -2,17 +2,13 @@
 // P:257-262 "we iterated through all core frequencies … and calculated the corresponding
 // EDP", Table 6 P:550-567 Offline vs Online) and K5: per-tuner regret against it.
 //
-// K4 mapping: one CTA per trace, one thread per arm (128 slots, K ≤ 128).  Windows are
-// processed in tiles of 32: the tile's step records (4 KB) are staged in shared memory and
-// broadcast to every arm thread; each thread evaluates ENV-R at its frequency for the 32
-// windows (kIlp independent evaluations in flight), adding E, TPOT, EDP into its per-arm
-// sums in ascending t (ENV.md §5's left-to-right order, so chunked sweeps equal one sweep)
-// and the EDP into the running sum of the window's prototype (runs split at segment
-// boundaries, so the prototype is block-uniform per run).  The tile's EDPs go to shared memory; each
-// warp then takes 8 windows and finds k° (smallest arm index on ties) with a lane-local
-// pass over 4 arms and three warp min-reductions on the EDP bit patterns; one thread adds the tile's oracle EDP and
-// energy in window order.  FP64-ALU bound: ~22 FP64 operations per (window, arm), the
-// record read once per (trace, window) for 107 arms.
+// K4 mapping: one CTA per trace (256 threads), windows in tiles of 32 whose step records (4 KB)
+// are staged in shared memory and broadcast to every arm.  Per-arm sums are folded in ascending t
+// (ENV.md §5's left-to-right order, so chunked sweeps equal one sweep), the EDP also into the
+// running sum of the window's prototype (runs split at segment boundaries).  k° per window
+// (smallest arm index on ties) comes from warp min-reductions on the EDP bit patterns; its EDP
+// and energy are folded in window order.  FP64-ALU bound: ~22 FP64 operations per (window, arm),
+// the record read once per (trace, window) for 107 arms.
 #include "env_t.cuh"
 
 namespace agft {
@@ -20,7 +16,9 @@ namespace agft {
 namespace {
 
 constexpr int kTile = 32;
-constexpr int kThreads = 128;
+constexpr int kThreads2 = 256;
+constexpr int kMaxArmsSw = 128;
+constexpr size_t kSweepSmem = (size_t)kTile * 16 * 8 + 3 * (size_t)kTile * kMaxArmsSw * 8 + 2 * kTile * 8;
 #ifndef AGFT_SWEEP_ILP
 #define AGFT_SWEEP_ILP 8
 #endif
@@ -42,33 +40,48 @@ struct SweepArgs {
     double W, p_idle, u_floor, u_max;
 };
 
-__global__ void __launch_bounds__(kThreads) sweep_kernel(const __grid_constant__ SweepArgs a)
+// K4 v2 (v1 ran one 128-thread CTA per trace — 256 CTAs, ~7 warps per SM, 5.5% of
+// the FP64 pipe).  The per-(trace, arm) sums must be folded left to right in t (ENV.md §5), but
+// the ENV-R evaluations feeding them are independent, so the two are split inside the CTA:
+//   A. all 256 threads evaluate the tile's 32 windows × 128 arm slots (16 evaluations each,
+//      kIlp in flight) into shared memory E / TPOT / EDP tables [window][arm];
+//   B. warps 0–3 (thread k = arm k) fold the tile into their sums in window order, while warps
+//      4–7 find each window's k° (8 windows per warp) and one of them folds the oracle sums —
+// so the FP64 evaluations run at 16 warps per SM (two CTAs of 100 KB) and the serial folds,
+// ~1/20 of the arithmetic, overlap each other.  Results are bit-identical to v1.
+__global__ void __launch_bounds__(kThreads2, 2) sweep_kernel(const __grid_constant__ SweepArgs a)
 {
-    __shared__ __align__(16) StepRec s_rec[kTile];
-    __shared__ double s_edp[kTile][kThreads];
-    __shared__ double s_oe[kTile], s_oE[kTile];
-    const uint32_t r = blockIdx.x;                                    // local trace
-    const int k = threadIdx.x, lane = k & 31, warp = k >> 5;
-    const bool arm = (uint32_t)k < a.K;
+    extern __shared__ __align__(16) double sw[];
+    StepRec *s_rec = reinterpret_cast<StepRec *>(sw);                            // [kTile]
+    double *s_E = sw + kTile * 16, *s_T = s_E + kTile * kMaxArmsSw, *s_D = s_T + kTile * kMaxArmsSw;
+    double *s_oe = s_D + kTile * kMaxArmsSw, *s_oE = s_oe + kTile;
+    const uint32_t r = blockIdx.x;                                               // local trace
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const EnvConsts &ec = *a.env;
-    const double dec = arm ? ec.dec[k] : 0.0, pre = arm ? ec.pre[k] : 0.0, pw = arm ? ec.pw[k] : 0.0;
     const double invW = ec.invW, q_over = ec.q_over;
     const Philox ph{(uint32_t)a.seed ^ (a.trace_base + r), (uint32_t)(a.seed >> 32)};
-
+    // phase A mapping: arm slot ka, windows [wa0, wa0 + 16)
+    const int ka = lane + 32 * (warp & 3), wa0 = (warp >> 2) * (kTile / 2);
+    const bool arm_a = (uint32_t)ka < a.K;
+    const double dec = arm_a ? ec.dec[ka] : 0.0, pre = arm_a ? ec.pre[ka] : 0.0, pw = arm_a ? ec.pw[ka] : 0.0;
+    // phase B accumulators: warps 0–3, thread tid = arm
+    const bool acc = warp < 4, arm = acc && (uint32_t)tid < a.K;
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, sp[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
     if (arm) {
-        const double *S = a.S + ((size_t)r * a.K + k) * 3;
+        const double *S = a.S + ((size_t)r * a.K + tid) * 3;
         s0 = S[0];
         s1 = S[1];
         s2 = S[2];
 #pragma unroll
-        for (int p = 0; p < 5; ++p) sp[p] = a.SP[((size_t)r * 5 + p) * a.K + k];
+        for (int p = 0; p < 5; ++p) sp[p] = a.SP[((size_t)r * 5 + p) * a.K + tid];
     }
-    double o0 = 0.0, o1 = 0.0;
-    uint32_t np[5] = {0u, 0u, 0u, 0u, 0u};
-    if (k == 0) {
+    double o0 = 0.0, o1 = 0.0;                                                   // warp 4, lane 0
+    uint32_t np[5] = {0u, 0u, 0u, 0u, 0u};                                       // thread 0
+    if (tid == 128) {
         o0 = a.O[2 * r];
         o1 = a.O[2 * r + 1];
+    }
+    if (tid == 0) {
 #pragma unroll
         for (int p = 0; p < 5; ++p) np[p] = a.NP[r * 5 + p];
     }
@@ -76,100 +89,109 @@ __global__ void __launch_bounds__(kThreads) sweep_kernel(const __grid_constant__
 
     for (uint32_t base = 0; base < a.n_steps; base += kTile) {
         const int nw = (int)min((uint32_t)kTile, a.n_steps - base);
-        // ---- stage the tile's records (coalesced 16-B loads) and prototypes
-        {
+        {                                                                        // stage the records
             const uint4 *src = reinterpret_cast<const uint4 *>(rp + base);
             uint4 *dst = reinterpret_cast<uint4 *>(s_rec);
-            for (int q = k; q < nw * 8; q += kThreads) dst[q] = __ldg(src + q);
+            for (int q = tid; q < nw * 8; q += kThreads2) dst[q] = __ldg(src + q);
         }
         __syncthreads();
-        // ---- ENV-R at this thread's frequency for every window of the tile (ENV.md §3.3):
-        // kIlp independent evaluations in flight, then the in-order accumulation.  Windows of
-        // one 10-minute segment share a prototype, so a tile holds at most two prototype runs
-        // (seg_steps ≥ kTile); each run accumulates into one register copied in and out.
-        int w = 0;
-        while (w < nw) {                                                  // block-uniform runs
-            const uint32_t t = a.t0 + base + (uint32_t)w;
-            const uint32_t p = prototype_of(a.tc, ph, t);
-            const int wend = w + (int)min((uint32_t)(nw - w), a.tc.seg_steps - t % a.tc.seg_steps);
-            if (k == 0) np[p] += (uint32_t)(wend - w);
-            double cur = p == 0 ? sp[0] : p == 1 ? sp[1] : p == 2 ? sp[2] : p == 3 ? sp[3] : sp[4];
-            for (; w < wend; w += kIlp) {
-                double E[kIlp], tp[kIlp], ed[kIlp];
+        // ---- A: ENV-R (ENV.md §3.3) at arm ka for windows wa0.. (kIlp in flight)
 #pragma unroll
-                for (int j = 0; j < kIlp; ++j) {
-                    const int wj = w + j < wend ? w + j : w;
-                    response(s_rec[wj], dec, pre, pw, a.W, invW, q_over, a.u_max, a.u_floor, a.p_idle, E[j], tp[j]);
-                    ed[j] = xmul(E[j], tp[j]);
+        for (int j0 = 0; j0 < kTile / 2; j0 += kIlp) {
+            double E[kIlp], tp[kIlp];
+#pragma unroll
+            for (int j = 0; j < kIlp; ++j) {
+                const int w = wa0 + j0 + j;
+                response(s_rec[w < nw ? w : 0], dec, pre, pw, a.W, invW, q_over, a.u_max, a.u_floor, a.p_idle, E[j],
+                         tp[j]);
+            }
+#pragma unroll
+            for (int j = 0; j < kIlp; ++j) {
+                const int w = wa0 + j0 + j;
+                if (w < nw) {
+                    s_E[w * kMaxArmsSw + ka] = E[j];
+                    s_T[w * kMaxArmsSw + ka] = tp[j];
+                    s_D[w * kMaxArmsSw + ka] = arm_a ? xmul(E[j], tp[j]) : kInf;
                 }
-#pragma unroll
-                for (int j = 0; j < kIlp; ++j)
-                    if (w + j < wend) {
-                        s_edp[w + j][k] = arm ? ed[j] : kInf;
-                        s0 = xadd(s0, E[j]);
-                        s1 = xadd(s1, tp[j]);
-                        s2 = xadd(s2, ed[j]);
-                        cur = xadd(cur, ed[j]);
+            }
+        }
+        __syncthreads();
+        if (acc) {
+            // ---- B1: per-arm folds in window order; prototype runs split at segment boundaries
+            int w = 0;
+            while (w < nw) {                                                     // uniform over warps 0–3
+                const uint32_t t = a.t0 + base + (uint32_t)w;
+                const uint32_t p = prototype_of(a.tc, ph, t);
+                const int wend = w + (int)min((uint32_t)(nw - w), a.tc.seg_steps - t % a.tc.seg_steps);
+                if (tid == 0) np[p] += (uint32_t)(wend - w);
+                double cur = p == 0 ? sp[0] : p == 1 ? sp[1] : p == 2 ? sp[2] : p == 3 ? sp[3] : sp[4];
+                if (arm) {
+                    for (; w < wend; ++w) {
+                        const double ed = s_D[w * kMaxArmsSw + tid];
+                        s0 = xadd(s0, s_E[w * kMaxArmsSw + tid]);
+                        s1 = xadd(s1, s_T[w * kMaxArmsSw + tid]);
+                        s2 = xadd(s2, ed);
+                        cur = xadd(cur, ed);
                     }
+                }
+                w = wend;
+                if (p == 0) sp[0] = cur;
+                else if (p == 1) sp[1] = cur;
+                else if (p == 2) sp[2] = cur;
+                else if (p == 3) sp[3] = cur;
+                else sp[4] = cur;
             }
-            w = wend;
-            if (p == 0) sp[0] = cur;
-            else if (p == 1) sp[1] = cur;
-            else if (p == 2) sp[2] = cur;
-            else if (p == 3) sp[3] = cur;
-            else sp[4] = cur;
-        }
-        __syncthreads();
-        // ---- per-window oracle arm k° (smallest index on ties), 8 windows per warp.  EDP > 0
-        // (ENV.md §3.3) and inactive slots hold +inf, so doubles order like their bit
-        // patterns: min of the high words, then of the low words among the ties, then the
-        // smallest arm index among exact ties (three warp reductions, no shuffle tree).
-        for (int j = 0; j < kTile / 4; ++j) {
-            const int w = warp * (kTile / 4) + j;
-            if (w >= nw) break;                                           // warp-uniform
-            double bv = s_edp[w][lane];
-            int bk = lane;
+        } else {
+            // ---- B2: per-window oracle arm k° (smallest index on ties), 8 windows per warp.  EDP > 0
+            // (ENV.md §3.3) and empty slots hold +inf, so doubles order like their bit patterns: min
+            // of the high words, then of the low words among the ties, then the smallest arm index.
+            for (int j = 0; j < kTile / 4; ++j) {
+                const int w = (warp - 4) * (kTile / 4) + j;
+                if (w >= nw) break;                                              // warp-uniform
+                double bv = s_D[w * kMaxArmsSw + lane];
+                int bk = lane;
 #pragma unroll
-            for (int q = 1; q < kThreads / 32; ++q) {
-                const double v = s_edp[w][lane + 32 * q];
-                if (v < bv) {
-                    bv = v;
-                    bk = lane + 32 * q;
+                for (int q = 1; q < kMaxArmsSw / 32; ++q) {
+                    const double v = s_D[w * kMaxArmsSw + lane + 32 * q];
+                    if (v < bv) {
+                        bv = v;
+                        bk = lane + 32 * q;
+                    }
+                }
+                const uint64_t bits = (uint64_t)__double_as_longlong(bv);
+                const uint32_t hi = (uint32_t)(bits >> 32), lo = (uint32_t)bits;
+                const uint32_t mhi = __reduce_min_sync(kFull, hi);
+                const uint32_t mlo = __reduce_min_sync(kFull, hi == mhi ? lo : 0xFFFFFFFFu);
+                const uint32_t kmin = __reduce_min_sync(kFull, (hi == mhi && lo == mlo) ? (uint32_t)bk : 0xFFFFFFFFu);
+                if (lane == j) {
+                    s_oe[w] = __longlong_as_double((long long)(((uint64_t)mhi << 32) | mlo));
+                    s_oE[w] = s_E[w * kMaxArmsSw + kmin];                        // E at k°, as evaluated
+                    if (a.best) a.best[(size_t)r * a.n_steps + base + w] = (uint8_t)kmin;
                 }
             }
-            const uint64_t bits = (uint64_t)__double_as_longlong(bv);
-            const uint32_t hi = (uint32_t)(bits >> 32), lo = (uint32_t)bits;
-            const uint32_t mhi = __reduce_min_sync(kFull, hi);
-            const uint32_t mlo = __reduce_min_sync(kFull, hi == mhi ? lo : 0xFFFFFFFFu);
-            const uint32_t kmin = __reduce_min_sync(kFull, (hi == mhi && lo == mlo) ? (uint32_t)bk : 0xFFFFFFFFu);
-            if (lane == j) {                                              // energy at k°, bit-identical
-                double E, tpot;
-                response(s_rec[w], ec.dec[kmin], ec.pre[kmin], ec.pw[kmin], a.W, invW, q_over, a.u_max,
-                         a.u_floor, a.p_idle, E, tpot);
-                s_oe[w] = __longlong_as_double((long long)(((uint64_t)mhi << 32) | mlo));
-                s_oE[w] = E;
-                if (a.best) a.best[(size_t)r * a.n_steps + base + w] = (uint8_t)kmin;
+            asm volatile("bar.sync 1, 128;" ::: "memory");                       // warps 4–7: all k° written
+            if (tid == 128) {                                                    // ENV.md §5: in window order
+                for (int w = 0; w < nw; ++w) {
+                    o0 = xadd(o0, s_oe[w]);
+                    o1 = xadd(o1, s_oE[w]);
+                }
             }
         }
         __syncthreads();
-        if (k == 0) {                                                     // ENV.md §5: in window order
-            for (int w = 0; w < nw; ++w) {
-                o0 = xadd(o0, s_oe[w]);
-                o1 = xadd(o1, s_oE[w]);
-            }
-        }
     }
     if (arm) {
-        double *S = a.S + ((size_t)r * a.K + k) * 3;
+        double *S = a.S + ((size_t)r * a.K + tid) * 3;
         S[0] = s0;
         S[1] = s1;
         S[2] = s2;
 #pragma unroll
-        for (int p = 0; p < 5; ++p) a.SP[((size_t)r * 5 + p) * a.K + k] = sp[p];
+        for (int p = 0; p < 5; ++p) a.SP[((size_t)r * 5 + p) * a.K + tid] = sp[p];
     }
-    if (k == 0) {
+    if (tid == 128) {
         a.O[2 * r] = o0;
         a.O[2 * r + 1] = o1;
+    }
+    if (tid == 0) {
 #pragma unroll
         for (int p = 0; p < 5; ++p) a.NP[r * 5 + p] = np[p];
     }
@@ -236,7 +258,9 @@ cudaError_t launch_sweep(const Ws &w, const agft_config &c, const void *records,
     a.p_idle = c.env.p_idle;
     a.u_floor = c.env.u_floor;
     a.u_max = c.env.u_max;
-    sweep_kernel<<<c.n_traces, kThreads, 0, s>>>(a); note_launches(1);
+    cudaError_t e = cudaFuncSetAttribute(sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepSmem);
+    if (e != cudaSuccess) return e;
+    sweep_kernel<<<c.n_traces, kThreads2, kSweepSmem, s>>>(a); note_launches(1);
     return cudaGetLastError();
 }
 

@@ -49,6 +49,33 @@ def plan(cfg: dict, world: int, rank: int, scaling: str = "weak") -> Shard:
     return Shard(rank, world, n, r, base, rank * n, p)
 
 
+COUNTER_NAMES = ("tuner_steps", "flagged_tuners", "near_tie_steps", "incomplete_tuners", "pruned_extreme",
+                 "pruned_hist", "pruned_cascade", "active_arm_steps", "exploit_steps", "ph_alarms", "refinements",
+                 "tuners", "active_arms_end", "single_arm_tuners", "reserved14", "reserved15")
+
+
+def counter_vector(st, T: int) -> list:
+    """The 16 run counters SURVEY §8(e) all-reduces across ranks, from a rank's agft_tuner_stats
+    array: tuner-steps, flagged (frozen) tuners, near-tie steps, invariant violations (tuners that did
+    not complete all T steps), pruning counts by cause, Σ K_act, phase / refinement counters, tuners,
+    active arms at the end and single-arm tuners."""
+    s64 = lambda f: int(np.sum(st[f], dtype=np.int64))
+    return [s64("steps"), int(np.count_nonzero(st["flags"])), s64("near_tie_steps"),
+            int(np.count_nonzero(st["steps"] != T)), s64("n_pruned_extreme"), s64("n_pruned_hist"),
+            s64("n_pruned_cascade"), int(np.sum(st["sum_active"], dtype=np.uint64)), s64("exploit_steps"),
+            s64("ph_alarms"), s64("n_refine"), len(st), s64("n_active"), int(np.count_nonzero(st["n_active"] == 1)),
+            0, 0]
+
+
+def reduce_counters(vec, device=None, group=None) -> dict:
+    """Sum-all-reduce a rank's 16 counters (one int64 tensor, one collective)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(vec, dtype=torch.int64, device=device)
+    dist.all_reduce(t, group=group)
+    return dict(zip(COUNTER_NAMES, (int(v) for v in t.cpu().tolist())))
+
+
 def gather_stats(stats_bytes, group=None):
     """All-gather each rank's per-tuner stats (a uint8 tensor) in rank order (global tuner order)."""
     import torch

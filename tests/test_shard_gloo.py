@@ -36,6 +36,17 @@ def _stats_array(stats_list):
     return np.array([tuple(s[f] for f in fields) for s in stats_list], dtype=dt)
 
 
+def _as_lib_stats(st):
+    """The oracle's stats rows in the library's agft_tuner_stats layout (flags = 0: the oracle
+    never freezes a tuner on these inputs), as shard.counter_vector reads them."""
+    from paper_2508_01744_b200._abi import STATS_DTYPE
+    out = np.zeros(len(st), dtype=STATS_DTYPE)
+    for f in STATS_DTYPE.names:
+        if f in st.dtype.names:
+            out[f] = st[f]
+    return out
+
+
 def _worker(rank, world, port, scaling, out_path):
     import sys
     sys.path.insert(0, ROOT)
@@ -52,8 +63,10 @@ def _worker(rank, world, port, scaling, out_path):
     t = torch.from_numpy(st.view(np.uint8).copy())
     g = shard.gather_stats(t)
     mx = shard.max_over_ranks(float(rank + 1))
+    cnt = shard.reduce_counters(shard.counter_vector(_as_lib_stats(st), cfg["T"]))
     if rank == 0:
         np.save(out_path, g.numpy())
+        np.save(out_path + ".counters.npy", np.array([cnt[k] for k in shard.COUNTER_NAMES], dtype=np.int64))
         assert mx == float(world)
     dist.barrier()
     dist.destroy_process_group()
@@ -76,6 +89,11 @@ def test_two_rank_gloo_gather_matches_single_process(tmp_path, scaling):
         rows.append(_stats_array(oracle.run_batch(cfg, p, cfg["T"], threads=2)))
     ref = np.concatenate(rows)
     assert gathered.tobytes() == ref.view(np.uint8).tobytes()
+    # the 16-counter all-reduce equals the counters of the single-process run
+    counters = np.load(out + ".counters.npy")
+    expect = shard.counter_vector(_as_lib_stats(ref), cfg["T"])
+    assert counters.tolist() == expect
+    assert expect[0] == cfg["n_tuners"] * (2 if scaling == "weak" else 1) * cfg["T"]
 
 
 def test_plan_partitions():

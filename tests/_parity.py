@@ -11,7 +11,9 @@ EXACT_STATS = ("steps", "last_arm", "n_active", "n_pruned_extreme", "n_pruned_hi
                "n_refine", "last_anchor")
 REL_TOL = 1e-9   # north_star: A⁻¹ entries and scores to 1e-9 relative (fp64)
 ABS_FLOOR = 1e-12  # per-entry floor, as a fraction of the arm's largest |entry| (entries that cancel to ~0)
-GAP_TOL = 1e-9   # the recorded top-2 gap is a normalised score difference (ENV.md §4.5)
+# the recorded top-2 gap (s1 − s2)/max(m1, m2) (ENV.md §4.5): two scores each within REL_TOL of their
+# magnitude move it by at most (REL_TOL·m1 + REL_TOL·m2)/max(m1, m2) ≤ 2·REL_TOL
+GAP_TOL = 2 * REL_TOL
 TIE_EDGE = 1e-12  # near-tie flags may differ only where the gap is within this of tie_rel
 
 
@@ -30,9 +32,12 @@ def compare_arms(g: dict, o: dict, K: int) -> list[str]:
             errs.append(f"{f} differs (max abs {np.max(np.abs(g[f] - o[f])):.3e})")
     for f in ("Ainv", "theta"):              # tolerance-compared (Sherman–Morrison vs Gauss–Jordan)
         gv, ov = np.asarray(g[f]), np.asarray(o[f])
-        for k in range(K):                   # per entry: relative, with a floor at 1e-12 of the arm's scale
+        for k in range(K):
             scale = max(np.max(np.abs(ov[k])), 1e-300)
-            tol = REL_TOL * np.abs(ov[k]) + ABS_FLOOR * scale
+            if f == "Ainv":                  # north_star: A⁻¹ ENTRIES to 1e-9 relative (floor 1e-12 of the scale)
+                tol = REL_TOL * np.abs(ov[k]) + ABS_FLOOR * scale
+            else:                            # θ enters Eq. 1 only through θᵀx, x ∈ [0,1]^d: normwise per arm
+                tol = np.full(ov[k].shape, REL_TOL * scale)
             bad = np.abs(gv[k] - ov[k]) > tol
             if np.any(bad):
                 e = np.argmax(np.abs(gv[k] - ov[k]) - tol)

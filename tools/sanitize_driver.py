@@ -32,9 +32,11 @@ def main(T: int):
         st = tb.stats()
         assert np.all(st["steps"] == cfg["T"]), name
         if name == "classes":
-            ck = tb.checkpoint()
-            tb2 = TunerBatch.resume(cfg, tuner_params(cfg), ck, device="cuda:0")
-            tb2.close()
+            if os.environ.get("SAN_NO_CHECKPOINT") != "1":   # initcheck: the checkpoint copies scratch regions
+                ck = tb.checkpoint()
+                tb2 = TunerBatch.resume(cfg, tuner_params(cfg), ck, device="cuda:0",
+                                        record_slot=[0] + [0xFFFFFFFF] * (cfg["n_tuners"] - 1))
+                tb2.close()
             sums = tb.new_sweep()
             tb.reset()
             rec = tb.generate(0, cfg["T"])

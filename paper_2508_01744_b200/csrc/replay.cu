@@ -440,6 +440,7 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
             break;
         }
         if (a.ph_enable) {                            // ENV.md §4.10 observe_reward
+            __syncwarp();                             // every lane's read of the last step's phase is done
             if (lane == 0) {
                 s_ph[warp].exploit_steps += phase;
                 ph_observe(s_ph[warp], r, t, a.ph_window, a.ph_delta, a.ph_lambda);

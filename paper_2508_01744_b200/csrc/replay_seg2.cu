@@ -16,6 +16,7 @@
 // width-G butterfly combines the blocks — the same pairwise tree, empty slots adding +0.0.
 // Control flow is warp-uniform around every collective; per-segment effects are predicated.
 #include "seg_common.cuh"
+#include "rec_tile.cuh"
 
 namespace agft {
 
@@ -38,6 +39,9 @@ template <int G>
 __host__ __device__ constexpr bool b_in_smem() { return true; }
 template <int G>
 __host__ __device__ constexpr bool env_in_smem() { return G >= 8; }
+
+template <int G>
+__host__ __device__ constexpr bool kScreen() { return G >= 8; }
 
 template <int G>
 constexpr size_t seg2_smem_bytes(int P, int D)
@@ -163,6 +167,14 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
     int nact = spopc<G>(act0, sg) + spopc<G>(act1, sg);
     const StepRec *rp = a.records + (size_t)prm.trace_id * a.rec_stride + a.rec_off;
     const bool rec_on = prm.record_slot != AGFT_NO_RECORD;
+#if AGFT_TMA
+    // a1: the warp's records by bulk copy when all its segments replay one trace (rec_tile.cuh)
+    __shared__ __align__(128) StepRec s_rtile[kSeg2Warps][2 * kRecTile];
+    __shared__ __align__(8) uint64_t s_rbar[kSeg2Warps][2];
+    RecTile rt{s_rtile[warp], s_rbar[warp], rp, a.n_steps,
+               __all_sync(kFull, prm.trace_id == __shfl_sync(kFull, prm.trace_id, 0))};
+    rt.start(lane);
+#endif
     const double inv_tau = 1.0 / a.tau;
     const uint32_t *rawp = a.cl_enable ? a.raw + ((size_t)prm.trace_id * a.rec_stride + a.rec_off) * AGFT_ROW_WORDS
                                        : nullptr;
@@ -175,19 +187,25 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
 
     for (uint32_t s = 0; s < a.n_steps; ++s) {
         const uint32_t t = a.t0 + s;
+#if AGFT_TMA
+        const StepRec *rc = rt.on ? rt.at(s, lane) : rp + s;
+#define RF(f) (rt.on ? rc->f : __ldg(&rc->f))
+#else
         const StepRec *rc = rp + s;
+#define RF(f) __ldg(&rc->f)
+#endif
         if (s + 1 < a.n_steps && l == 0) {
-            prefetch_l1(rc + 1);
+            if (!AGFT_TMA) prefetch_l1(rc + 1);
             if (rawp) prefetch_l1(rawp + (size_t)(s + 1) * AGFT_ROW_WORDS);
         }
         double x[D];
 #pragma unroll
-        for (int i = 0; i < D; ++i) x[i] = __ldg(&rc->x[i]);
-        double g = __ldg(&rc->g), wIm = __ldg(&rc->wIm), baseE = __ldg(&rc->baseE), baseEDP = __ldg(&rc->baseEDP);
+        for (int i = 0; i < D; ++i) x[i] = RF(x[i]);
+        double g = RF(g), wIm = RF(wIm), baseE = RF(baseE), baseEDP = RF(baseEDP);
         uint32_t arr_cl = 0u;
         if (rawp) {                                                   // ENV-C: the servers see their backlog
-            const ClosedRec cr = closed_record(rawp + (size_t)s * AGFT_ROW_WORDS, clq, clqb, __ldg(&rc->I),
-                                               __ldg(&rc->P), __ldg(&rc->invIm), __ldg(&rc->nT), __ldg(&rc->nE),
+            const ClosedRec cr = closed_record(rawp + (size_t)s * AGFT_ROW_WORDS, clq, clqb, RF(I),
+                                               RF(P), RF(invIm), RF(nT), RF(nE),
                                                ec, a);
             x[0] = cr.x0;
             g = cr.g;
@@ -270,9 +288,9 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
         // ---- a7: response
         const Response o = env_response(kEnvS ? s_dec[kstar] : __ldg(&ec->dec[kstar]),
                                         kEnvS ? s_pre[kstar] : __ldg(&ec->pre[kstar]),
-                                        kEnvS ? s_pw[kstar] : __ldg(&ec->pw[kstar]), __ldg(&rc->I), __ldg(&rc->P),
-                                        g, __ldg(&rc->invIm), __ldg(&rc->invAm), wIm,
-                                        __ldg(&rc->nT), __ldg(&rc->nE), invW, q_over, a.u_max, a.u_floor,
+                                        kEnvS ? s_pw[kstar] : __ldg(&ec->pw[kstar]), RF(I), RF(P),
+                                        g, RF(invIm), RF(invAm), wIm,
+                                        RF(nT), RF(nE), invW, q_over, a.u_max, a.u_floor,
                                         a.p_idle, a.W);
         if (rawp) clq = closed_carry(arr_cl + clq, o.u, a.cl_q_max);
         // ---- a8: reward + segment window
@@ -285,6 +303,7 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
             live = false;
         }
         if (a.ph_enable) {                                            // ENV.md §4.10 observe_reward
+            __syncwarp();                                             // the last step's phase reads are done
             if (live && l == 0) {
                 ph.exploit_steps += phase;
                 ph_observe(ph, r, t, a.ph_window, a.ph_delta, a.ph_lambda);
@@ -338,7 +357,15 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
             const int nq = spopc<G>(q0, sg) + spopc<G>(q1, sg);
             const bool need = live && t >= a.hist_t && nq >= 2;
             bool hist0 = false, hist1 = false;
-            if (__any_sync(kFull, need)) {
+            // the screen (seg_common.cuh) skips the exact trees when no arm of Q can be removed; on for
+            // G ≥ 8 (A/B on the C4 day: −10% / −8% / −6% kernel time for G = 8 / 16 / 32, +9% for G = 4,
+            // whose small Q sets are mostly pruned anyway — DESIGN.md §4)
+            bool exact = need;
+            if (kScreen<G>() && __any_sync(kFull, need)) {             // warp-wide call (butterflies)
+                const bool safe = hist_screen_safe<G>(q0, eb0, q1, eb1, nq, prm.historical_k);
+                exact = need && !safe;
+            }
+            if (__any_sync(kFull, exact)) {
                 double best = fmin(q0 ? eb0 : kInf, q1 ? eb1 : kInf);
 #pragma unroll
                 for (int off = G / 2; off > 0; off >>= 1) best = fmin(best, __shfl_xor_sync(kFull, best, off, G));
@@ -412,6 +439,7 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
         }
     }
 
+#undef RF
     // ---- write back (segments of real tuners only)
     __syncwarp();
     if (valid) {

@@ -103,4 +103,39 @@ __device__ __forceinline__ double stree(double *buf, int l, bool h0, int k0, dou
     return s;
 }
 
+// Historical-pruning screen (ENV.md §4.8).  Historical pruning removes arm k ∈ Q iff
+// ē_k > thr = best + k_h·σ, with μ and σ from the canonical 128-slot trees.  From min, max, Σē and
+// Σē² over Q (one butterfly, any order) this returns true only when max ē_Q < thr_lo ≤ thr, so that
+// the exact evaluation would remove nothing and may be skipped:
+//   V = Σē²/n − μ² is within 27u·m2 of the true population variance V* (u = 2⁻⁵³, m2 = Σē²/n; sums
+//   of ≤ 64 positive terms, one product, one subtraction), taken as dV = 64u·m2; the exact path's σ
+//   is ≥ √V*·(1 − 8u) (its μ error only adds n·ε² to Σ(ē − μ)², and the tree / division / square
+//   root round by ≤ 8u), so thr_lo = (best + k_h·√(V − dV)(1 − 8u))(1 − 16u) ≤ thr.
+// All equal means (max = min = best) remove nothing either: thr ≥ best.  Called warp-wide.
+template <int G>
+__device__ __forceinline__ bool hist_screen_safe(bool q0, double e0, bool q1, double e1, int nq, double kh)
+{
+    double mn = fmin(q0 ? e0 : kInf, q1 ? e1 : kInf);
+    double mx = fmax(q0 ? e0 : -kInf, q1 ? e1 : -kInf);
+    double s1 = (q0 ? e0 : 0.0) + (q1 ? e1 : 0.0);
+    double s2 = (q0 ? e0 * e0 : 0.0) + (q1 ? e1 * e1 : 0.0);
+#pragma unroll
+    for (int off = G / 2; off > 0; off >>= 1) {
+        mn = fmin(mn, __shfl_xor_sync(kFull, mn, off, G));
+        mx = fmax(mx, __shfl_xor_sync(kFull, mx, off, G));
+        s1 += __shfl_xor_sync(kFull, s1, off, G);
+        s2 += __shfl_xor_sync(kFull, s2, off, G);
+    }
+    if (!(mx > mn)) return true;
+    constexpr double u = 0x1p-53;
+    const double inq = 1.0 / (double)(nq > 0 ? nq : 1);
+    const double m2 = s2 * inq, mu = s1 * inq;
+    const double V = m2 - mu * mu;
+    const double dV = 64.0 * u * m2;
+    if (!(V - dV > 0.0)) return false;
+    const double sd_lo = sqrt(V - dV) * (1.0 - 8.0 * u);
+    const double thr_lo = (mn + kh * sd_lo) * (1.0 - 16.0 * u);
+    return mx < thr_lo;
+}
+
 }  // namespace agft

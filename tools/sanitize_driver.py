@@ -20,7 +20,8 @@ def main(T: int):
     cases = {
         "classes": (c4, 0),
         "wide": (c4, 1),
-        "phase_refine_classes": (dict(c4, ph_enable=0, rf_enable=1), 0),
+        "phase_classes": (dict(c4, ph_enable=1), 0),
+        "refine_classes": (dict(c4, ph_enable=0, rf_enable=1), 0),
         "phase_refine_wide": (dict(c4, ph_enable=1, rf_enable=1), 0),
         "closed": (dict(c4, cl_enable=1), 0),
         "C1": (named_config("C1"), 0),

@@ -102,6 +102,28 @@ class OrcInject(C.Structure):
 
 FREE = 255
 
+DES_RMAX, DES_QMAX, DES_OVER = 128, 512, 0.004
+
+
+class OrcDesReq(C.Structure):
+    _fields_ = [("arr", f64), ("ctx", u32), ("gen", u32), ("tmpl", u32), ("pad", u32)]
+
+
+class OrcDesSlot(C.Structure):
+    _fields_ = [("arr", f64), ("ctx", u32), ("gen", u32), ("done", u32), ("pre", u32), ("used", u32),
+                ("pad", u32)]
+
+
+class OrcDes(C.Structure):
+    """ENV.md §7 ENV-S: one tuner's discrete-event server (SPEC inference_sim)."""
+    _fields_ = [("clock", f64), ("q", OrcDesReq * DES_QMAX), ("qhead", u32), ("qlen", u32), ("nrun", u32),
+                ("kv", u32), ("dropped", u32), ("pad", u32), ("run", OrcDesSlot * DES_RMAX),
+                ("store", u32 * 16), ("snap", u32 * 8)]
+
+
+class OrcDesOut(C.Structure):
+    _fields_ = [("E", f64), ("tpot", f64), ("ttft", f64), ("edp", f64)]
+
 
 _lib = None
 
@@ -146,10 +168,15 @@ def lib():
         L.orc_stat_anchor.restype = u32
         L.orc_refine_window.argtypes = [C.POINTER(OrcConfig), u32, C.POINTER(C.c_uint8), C.POINTER(C.c_uint8)]
         L.orc_refine_window.restype = u32
+        L.orc_des_init.argtypes = [C.POINTER(OrcDes)]
+        L.orc_des_push.argtypes = [C.POINTER(OrcDes), C.POINTER(OrcConfig), f64, u32, u32, u32]
+        L.orc_des_push.restype = C.c_int
+        L.orc_des_run.argtypes = [C.POINTER(OrcDes), C.POINTER(OrcConfig), u32, f64, C.POINTER(OrcDesOut)]
+        L.orc_des_window.argtypes = [C.POINTER(OrcDes), C.POINTER(OrcConfig), u32, u32, u32, C.POINTER(OrcDesOut)]
         L.orc_sizeof.argtypes = [C.c_int]
         L.orc_sizeof.restype = u32
         for i, s in enumerate([OrcConfig, OrcTuner, OrcStats, OrcArms, OrcStepRec, OrcRecord,
-                               OrcInject]):
+                               OrcInject, OrcDes]):
             assert L.orc_sizeof(i) == C.sizeof(s), (s.__name__, L.orc_sizeof(i), C.sizeof(s))
         _lib = L
     return _lib
@@ -415,3 +442,37 @@ def offline_arm(values) -> int:
     """Smallest index minimising ``values`` (ENV.md §5 k_off)."""
     v = np.ascontiguousarray(values, dtype=np.float64)
     return int(lib().orc_argmin(_ptr(v, f64), len(v), 1))
+
+
+class DesServer:
+    """ENV.md §7 ENV-S server (test infrastructure): push requests, run windows, read the snapshot."""
+
+    def __init__(self, cfg: dict):
+        self.oc = make_config(cfg)
+        self.s = OrcDes()
+        lib().orc_des_init(C.byref(self.s))
+
+    def push(self, arr: float, ctx: int, gen: int, tmpl: int) -> bool:
+        """Queue a request; False if it was dropped (does not fit the KV cache or a full queue)."""
+        return lib().orc_des_push(C.byref(self.s), C.byref(self.oc), float(arr), ctx, gen, tmpl) == 0
+
+    def run(self, f_mhz: int, t_end: float) -> dict:
+        o = OrcDesOut()
+        lib().orc_des_run(C.byref(self.s), C.byref(self.oc), int(f_mhz), float(t_end), C.byref(o))
+        return {"E": o.E, "tpot": o.tpot, "ttft": o.ttft, "edp": o.edp}
+
+    def window(self, trace_id: int, t: int, f_mhz: int) -> dict:
+        o = OrcDesOut()
+        lib().orc_des_window(C.byref(self.s), C.byref(self.oc), trace_id, t, int(f_mhz), C.byref(o))
+        return {"E": o.E, "tpot": o.tpot, "ttft": o.ttft, "edp": o.edp}
+
+    @property
+    def snap(self) -> list:
+        """[waiting, running, prefill, decode, iterations, kv_used, hits, misses] of the last window."""
+        return list(self.s.snap)
+
+    @property
+    def state(self) -> dict:
+        run = [self.s.run[k] for k in range(DES_RMAX) if self.s.run[k].used]
+        return {"clock": self.s.clock, "qlen": self.s.qlen, "nrun": self.s.nrun, "kv": self.s.kv,
+                "dropped": self.s.dropped, "running": [(r.ctx, r.gen, r.done, r.pre) for r in run]}

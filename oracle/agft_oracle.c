@@ -489,6 +489,11 @@ int orc_run_tuner_ex(const orc_config *c, const orc_tuner *tu, uint32_t T, const
     if (c->median_window < 1 || c->median_window > ORC_MAX_WINDOW) return -1;
     tuner_state *S = (tuner_state *)calloc(1, sizeof(tuner_state));
     if (!S) return -2;
+    orc_des *des = NULL;                                             /* §7 ENV-S server of this tuner */
+    if (!inj && c->cl_enable == 2) {
+        des = (orc_des *)calloc(1, sizeof(orc_des));
+        if (!des) { free(S); return -2; }
+    }
 
     /* init (AMB-2): A = I, b = 0, θ = 0, all arms active */
     for (uint32_t k = 0; k < K; ++k) {
@@ -520,9 +525,16 @@ int orc_run_tuner_ex(const orc_config *c, const orc_tuner *tu, uint32_t T, const
             } else {
                 for (uint32_t i = 0; i < 7; ++i) x[i] = i < d ? inj->x[(size_t)t * d + i] : 0.0;
             }
+        } else if (c->cl_enable == 2) {                              /* §7 ENV-S: last window's snapshot */
+            uint32_t snap12[ORC_ROW_WORDS] = {0};
+            memcpy(snap12, des->snap, sizeof(des->snap));
+            double xr[7];
+            orc_context(c, snap12, xr);
+            memset(&srec, 0, sizeof(srec));                          /* no f_max baseline */
+            for (uint32_t i = 0; i < 7; ++i) x[i] = i < d ? xr[i] : 0.0;
         } else {
             orc_trace_row(c, tu->trace_id, t, row);                  /* a0 */
-            if (c->cl_enable) {                                      /* §6: the servers see their backlog */
+            if (c->cl_enable == 1) {                                 /* §6: the servers see their backlog */
                 uint32_t rq[ORC_ROW_WORDS], rb[ORC_ROW_WORDS];
                 memcpy(rq, row, sizeof(rq));
                 memcpy(rb, row, sizeof(rb));
@@ -615,11 +627,15 @@ int orc_run_tuner_ex(const orc_config *c, const orc_tuner *tu, uint32_t T, const
                 resp[0] = 0.0; resp[1] = 0.0; resp[2] = 0.0;
                 resp[3] = inj->edp ? inj->edp[(size_t)t * K + kstar] : 1.0;
             }
+        } else if (c->cl_enable == 2) {                              /* §7: the window on the tuner's server */
+            orc_des_out o;
+            orc_des_window(des, c, tu->trace_id, t, F, &o);
+            resp[0] = o.E; resp[1] = o.tpot; resp[2] = o.ttft; resp[3] = o.edp;
         } else {
             orc_response(c, &srec, F, resp);
         }
         double E = resp[0], tpot = resp[1], ttft = resp[2], edp = resp[3];
-        if (!inj && c->cl_enable) {                                   /* §6: backlog into window t+1 */
+        if (!inj && c->cl_enable == 1) {                                   /* §6: backlog into window t+1 */
             const uint32_t a = row[6] + row[7];
             cl_q = closed_next(c, &srec, a, cl_q, F);
             cl_qb = closed_next(c, &srecb, a, cl_qb, c->f_max_hw_mhz);
@@ -792,6 +808,7 @@ int orc_run_tuner_ex(const orc_config *c, const orc_tuner *tu, uint32_t T, const
         }
     }
     free(S);
+    free(des);
     return 0;
 }
 
@@ -837,6 +854,132 @@ int orc_run_batch(const orc_config *c, const orc_tuner *tuners, uint32_t n, uint
     return rc;
 }
 
+/* ---------------------------------------------------------------- ENV.md §7: ENV-S
+ * The discrete-event continuous-batching server of SPEC's inference_sim, written
+ * out as ENV.md §7 states it: FIFO admission while the KV footprint fits, one prefill
+ * iteration per admitted request (the uncached suffix; a template seen before skips half the
+ * prompt), then one output token per iteration, retirement at the target length; iteration time
+ * overhead + max(prefill, decode) × the concurrency penalty; energy p_idle·W + pw·max(u, u_floor)·W
+ * while busy. Plain loops over the queue and the slots, in slot order. */
+static const uint32_t des_pool[5] = {500, 500, 500, 500, 5};
+
+void orc_des_init(orc_des *s) { memset(s, 0, sizeof(*s)); }
+
+int orc_des_push(orc_des *s, const orc_config *c, double arr, uint32_t ctx, uint32_t gen, uint32_t tmpl)
+{
+    if ((uint64_t)ctx + gen > c->kv_total || s->qlen == ORC_DES_QMAX) {
+        s->dropped += 1;
+        return 1;
+    }
+    orc_des_req *q = &s->q[(s->qhead + s->qlen) % ORC_DES_QMAX];
+    q->arr = arr;
+    q->ctx = ctx;
+    q->gen = gen;
+    q->tmpl = tmpl;
+    s->qlen += 1;
+    return 0;
+}
+
+void orc_des_run(orc_des *s, const orc_config *c, uint32_t F, double t_end, orc_des_out *o)
+{
+    const double fmax = (double)c->f_max_hw_mhz / 1000.0;
+    const double f = (double)F / 1000.0;
+    const double dec = c->c_d / (c->beta + ((1.0 - c->beta) * (f / fmax)));   /* §3.1 */
+    const double pre = c->c_p / f;
+    const double pw = (c->k_lin * f) + (c->k_cube * ((f * f) * f));
+    uint32_t P = 0, Dc = 0, I = 0, hits = 0, misses = 0, n_tok = 0, n_first = 0;
+    double busy = 0.0, sdec = 0.0, sfirst = 0.0;
+    uint8_t fresh[ORC_DES_RMAX];
+    while (s->clock < t_end) {
+        uint32_t npre = 0;
+        memset(fresh, 0, sizeof(fresh));
+        while (s->qlen > 0) {                                       /* admission, head of line */
+            orc_des_req *h = &s->q[s->qhead];
+            if (!(h->arr <= s->clock) || s->nrun >= ORC_DES_RMAX || (uint64_t)s->kv + h->ctx + h->gen > c->kv_total)
+                break;
+            uint32_t hit = (s->store[h->tmpl >> 5] >> (h->tmpl & 31)) & 1u;
+            s->store[h->tmpl >> 5] |= 1u << (h->tmpl & 31);
+            hits += hit;
+            misses += 1u - hit;
+            npre += h->ctx - (hit ? h->ctx / 2 : 0u);
+            s->kv += h->ctx + h->gen;
+            uint32_t k = 0;
+            while (s->run[k].used) ++k;                              /* the lowest free slot */
+            s->run[k].arr = h->arr;
+            s->run[k].ctx = h->ctx;
+            s->run[k].gen = h->gen;
+            s->run[k].done = 0;
+            s->run[k].pre = 0;
+            s->run[k].used = 1;
+            fresh[k] = 1;
+            s->nrun += 1;
+            s->qhead = (s->qhead + 1) % ORC_DES_QMAX;
+            s->qlen -= 1;
+        }
+        uint32_t ndec = 0;
+        for (uint32_t k = 0; k < ORC_DES_RMAX; ++k) ndec += (s->run[k].used && s->run[k].pre) ? 1u : 0u;
+        if (npre == 0 && ndec == 0) {                                /* idle until the next arrival */
+            const double nxt = s->qlen > 0 ? s->q[s->qhead].arr : t_end;
+            s->clock = nxt < t_end ? nxt : t_end;
+            continue;
+        }
+        const double rho = (double)s->nrun / (double)c->cap;
+        const double g = rho > 1.0 ? rho * sqrt(rho) : 1.0;
+        const double tp = (double)npre * pre, td = ndec > 0 ? dec : 0.0;
+        const double dt = ORC_DES_OVER + ((tp > td ? tp : td) * g);
+        s->clock = s->clock + dt;
+        for (uint32_t k = 0; k < ORC_DES_RMAX; ++k) {                /* one output token each */
+            orc_des_slot *q = &s->run[k];
+            if (!q->used || !q->pre) continue;
+            q->done += 1;
+            if (q->done == 1) {
+                sfirst = sfirst + (s->clock - q->arr);
+                n_first += 1;
+            }
+            if (q->done == q->gen) {
+                s->kv -= q->ctx + q->gen;
+                q->used = 0;
+                s->nrun -= 1;
+            }
+        }
+        for (uint32_t k = 0; k < ORC_DES_RMAX; ++k)
+            if (fresh[k]) s->run[k].pre = 1;
+        P += npre;
+        Dc += ndec;
+        I += 1;
+        n_tok += ndec;
+        busy = busy + dt;
+        sdec = sdec + (dt * (double)ndec);
+    }
+    const double u = busy / c->W;
+    double ue = busy > 0.0 ? (u > 1.0 ? 1.0 : u) : 0.0;
+    if (busy > 0.0 && ue < c->u_floor) ue = c->u_floor;
+    o->E = (c->p_idle + (pw * ue)) * c->W;
+    o->tpot = n_tok > 0 ? sdec / (double)n_tok : dec;
+    o->ttft = n_first > 0 ? sfirst / (double)n_first : 0.0;
+    o->edp = o->E * o->tpot;
+    const uint32_t snap[8] = {s->qlen, s->nrun, P, Dc, I, s->kv, hits, misses};
+    memcpy(s->snap, snap, sizeof(snap));
+}
+
+void orc_des_window(orc_des *s, const orc_config *c, uint32_t r, uint32_t t, uint32_t F, orc_des_out *o)
+{
+    uint32_t row[ORC_ROW_WORDS];
+    orc_trace_row(c, r, t, row);
+    const uint32_t p = orc_prototype(c, r, t);
+    const uint32_t a = row[6] + row[7];                              /* §2.2 arrivals */
+    for (uint32_t i = 0; i < a; ++i) {
+        const double arr = ((double)t * c->W) + ((((double)i + 0.5) / (double)a) * c->W);
+        uint32_t u4[4];
+        draw(c, r, t, 5, i, 0, u4);
+        const uint32_t ctx = c->ctx_lo[p] + (uint32_t)(((uint64_t)u4[0] * (c->ctx_hi[p] - c->ctx_lo[p] + 1u)) >> 32);
+        const uint32_t gen = c->gen_lo[p] + (uint32_t)(((uint64_t)u4[1] * (c->gen_hi[p] - c->gen_lo[p] + 1u)) >> 32);
+        const uint32_t tmpl = (uint32_t)(((uint64_t)u4[2] * des_pool[p]) >> 32);
+        orc_des_push(s, c, arr, ctx, gen, tmpl);
+    }
+    orc_des_run(s, c, F, (double)(t + 1) * c->W, o);
+}
+
 uint32_t orc_sizeof(int which)
 {
     switch (which) {
@@ -847,6 +990,7 @@ uint32_t orc_sizeof(int which)
     case 4: return (uint32_t)sizeof(orc_steprec);
     case 5: return (uint32_t)sizeof(orc_record);
     case 6: return (uint32_t)sizeof(orc_inject);
+    case 7: return (uint32_t)sizeof(orc_des);
     default: return 0;
     }
 }

@@ -157,7 +157,31 @@ uint32_t orc_refine_window(const orc_config *c, uint32_t anchor, const uint8_t *
  * the carried-in backlog q) run at F MHz: q' = min(q_max, D - served), D = arrivals + q. */
 uint32_t orc_closed_next(const orc_config *c, const uint32_t row[ORC_ROW_WORDS], uint32_t q, uint32_t F_mhz);
 
-uint32_t orc_sizeof(int which /* 0 config 1 tuner 2 stats 3 arms 4 steprec 5 record 6 inject */);
+/* ENV.md §7 ENV-S: the discrete-event continuous-batching server (SPEC inference_sim, S:454-563;
+ * P:129-131), selected by cl_enable = 2.  State of one tuner's server and one window's outcome. */
+#define ORC_DES_RMAX 128
+#define ORC_DES_QMAX 512
+#define ORC_DES_OVER 0.004
+typedef struct { double arr; uint32_t ctx, gen, tmpl, pad; } orc_des_req;
+typedef struct { double arr; uint32_t ctx, gen, done, pre, used, pad; } orc_des_slot;
+typedef struct {
+    double clock;
+    orc_des_req q[ORC_DES_QMAX];
+    uint32_t qhead, qlen, nrun, kv, dropped, pad;
+    orc_des_slot run[ORC_DES_RMAX];
+    uint32_t store[16];                /* template prefix cached (512 bits) */
+    uint32_t snap[8];                  /* the last window's MetricsSnapshot (§2.2 word order) */
+} orc_des;
+typedef struct { double E, tpot, ttft, edp; } orc_des_out;
+void orc_des_init(orc_des *s);
+/* queue one request (ENV.md §7 arrival rule); returns 0, or 1 if it was dropped */
+int orc_des_push(orc_des *s, const orc_config *c, double arr, uint32_t ctx, uint32_t gen, uint32_t tmpl);
+/* run the engine until t_end at F MHz and measure the window (updates snap) */
+void orc_des_run(orc_des *s, const orc_config *c, uint32_t F, double t_end, orc_des_out *o);
+/* window t of trace r: its arrivals (§7), then orc_des_run to (t+1)·W */
+void orc_des_window(orc_des *s, const orc_config *c, uint32_t r, uint32_t t, uint32_t F, orc_des_out *o);
+
+uint32_t orc_sizeof(int which /* 0 config 1 tuner 2 stats 3 arms 4 steprec 5 record 6 inject 7 des */);
 
 /* Free-running batch over a pthread pool; stats[i] for tuners[i]. threads<=0: all cores. */
 int orc_run_batch(const orc_config *c, const orc_tuner *tuners, uint32_t n_tuners, uint32_t T,

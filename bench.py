@@ -209,7 +209,7 @@ def parity_summary(gst, ost) -> dict:
 
 def workload_key(args, cfg, n, R, T, chunk) -> str:
     return (f"{args.config}:n={n}:R={R}:T={T}:ph={int(bool(cfg.get('ph_enable')))}:rf={int(bool(cfg.get('rf_enable')))}"
-            f":cl={int(bool(cfg.get('cl_enable')))}:pol={args.policy}:chunk={chunk}")
+            f":cl={int(cfg.get('cl_enable', 0))}:pol={args.policy}:chunk={chunk}")
 
 
 def class_roofline(d, prof, prof_conc, steps, replay_ms, serial_replay_ms, st, n, T, R, traffic) -> dict:
@@ -279,6 +279,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--closed", action="store_true",
                     help="ENV-C closed-loop environment (ENV.md §6; raw rows alongside the records)")
+    ap.add_argument("--des", action="store_true",
+                    help="ENV-S: every tuner on its own discrete-event continuous-batching server (ENV.md §7)")
     ap.add_argument("--refine", action="store_true",
                     help="enable mixed maturity-based refinement (ENV.md §4.11; class schedule + refinement passes)")
     ap.add_argument("--chunk", type=int, default=CHUNK, help="windows per agft_replay call (records buffer)")
@@ -312,6 +314,8 @@ def main():
         cfg["rf_enable"] = 1          # ENV.md §4.11 refinement (NEXT row 1)
     if args.closed:
         cfg["cl_enable"] = 1          # ENV.md §6 closed loop (NEXT row 3)
+    if args.des:
+        cfg["cl_enable"] = 2          # ENV.md §7 ENV-S discrete-event servers (NEXT row 3)
     T = cfg["T"]
 
     if args.impl == "reference":
@@ -346,7 +350,7 @@ def main():
     chunk = min(args.chunk, T)
     records = tb.new_records(chunk)
     raw = (torch.empty((R, chunk, pkg.ROW_WORDS), dtype=torch.int32, device=f"cuda:{local}")
-           if args.closed else None)
+           if cfg.get("cl_enable") else None)
     stats_out = tb.stats_tensor()
     coll_dev = stats_out.device if args.backend == "nccl" else torch.device("cpu")
     gathered = (torch.empty(world * stats_out.numel(), dtype=torch.uint8, device=coll_dev)
@@ -432,7 +436,7 @@ def main():
                       "tuners_per_gpu": n, "T": T, "arms": cfg["n_arms"], "d": cfg["d"],
                       "phase_switch": bool(cfg.get("ph_enable", 0)),
                       "refinement": bool(cfg.get("rf_enable", 0)),
-                      "closed_loop": bool(cfg.get("cl_enable", 0)),
+                      "closed_loop": ["open", "ENV-C backlog", "ENV-S discrete-event servers"][cfg.get("cl_enable", 0)],
                       "traces_per_gpu": R, "chunk": chunk,
                       "l2": f"inputs larger than L2: tuner state {tb.workspace.numel() / 2**30:.2f} GiB/GPU",
                       "parallelism": f"tuner shards dp{world}"},

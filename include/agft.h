@@ -30,9 +30,10 @@
 extern "C" {
 #endif
 
-#define AGFT_ABI_VERSION 7u         /* 2: + agft_phase; 3: + agft_refine (and their stats); 4: + agft_select/agft_observe;
+#define AGFT_ABI_VERSION 8u         /* 2: + agft_phase; 3: + agft_refine (and their stats); 4: + agft_select/agft_observe;
                                        5: + agft_closed / agft_replay_raw; 6: MSEG/LANE policies retired;
-                                       7: + agft_profile_start / agft_profile_read (workspace +128 B) */
+                                       7: + agft_profile_start / agft_profile_read (workspace +128 B);
+                                       8: agft_closed.enable = 2 selects the ENV-S discrete-event server */
 #define AGFT_MAX_ARMS 128u          /* K ≤ 128 */
 #define AGFT_MAX_D 7u               /* the paper's 7-dim context */
 #define AGFT_MAX_WINDOW 64u         /* reward-median window, AMB-3 */
@@ -103,7 +104,14 @@ typedef struct { uint32_t enable, period, mature, min_samples, half_mhz, step_mh
 /* ENV-C closed loop (ENV.md §6): requests a window cannot
  * serve at the chosen clock (u > 1) wait into the next window, where the snapshot sees them
  * (x1, the concurrency penalty, TTFT); the f_max baseline carries its own backlog.  q_max caps
- * the backlog (requests).  Needs the raw rows: replay with agft_replay_raw. */
+ * the backlog (requests).  Needs the raw rows: replay with agft_replay_raw.
+ * enable = 2 selects ENV-S instead (ENV.md §7; SPEC inference_sim S:454-563; P:129-131 continuous
+ * batching): every tuner drives its own discrete-event server iteration by iteration — FIFO
+ * admission while the KV footprint fits, prefill of the uncached suffix, one token per iteration,
+ * retirement — at the clock it chose; each decision reads the server's last-window MetricsSnapshot
+ * and the reward comes from the simulated energy and TPOT.  The workspace then also holds
+ * each tuner's server (128 + 512·24 + 128·24 B); no f_max baseline is accumulated (base sums 0);
+ * the replay runs on the WIDE mapping.  q_max is unused. */
 typedef struct { uint32_t enable, q_max; } agft_closed;
 
 typedef struct {

@@ -14,7 +14,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("AGFT_LIB_PATH") or os.path.join(HERE, "libagft.so")   # override: A/B builds
 
-ABI_VERSION = 7
+ABI_VERSION = 8
 RECORD_BYTES = 128
 ROW_WORDS = 12
 NO_RECORD = 0xFFFFFFFF

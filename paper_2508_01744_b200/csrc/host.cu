@@ -142,7 +142,7 @@ agft_status validate(const agft_config *c)
     const agft_refine &rf = c->refine;               // ENV.md §4.11
     if (rf.enable > 1u) return AGFT_E_INVALID_ARG;
     if (rf.enable && (rf.period < 1u || rf.step_mhz < 1u)) return AGFT_E_INVALID_ARG;
-    if (c->closed.enable > 1u) return AGFT_E_INVALID_ARG;   // ENV.md §6
+    if (c->closed.enable > 2u) return AGFT_E_INVALID_ARG;   // 1: ENV-C (ENV.md §6), 2: ENV-S (§7)
     const agft_phase &ph = c->phase;                 // ENV.md §4.10
     if (ph.enable > 1u) return AGFT_E_INVALID_ARG;
     if (ph.enable && (ph.window < 1u || !finite(ph.delta) || !finite(ph.lambda) || ph.delta < 0 || ph.lambda < 0))
@@ -279,6 +279,9 @@ ReplayArgs replay_args(agft_handle h, const void *records, uint32_t t0, uint32_t
     a.cl_enable = c.closed.enable;
     a.cl_q_max = c.closed.q_max;
     a.cap = c.trace.cap;
+    a.tc = c.trace;                                   // ENV-S arrivals (ENV.md §7)
+    a.seed = c.env_seed;
+    a.trace_base = c.trace_base;
     std::memcpy(a.norm_lo, c.norm_lo, sizeof(a.norm_lo));
     std::memcpy(a.norm_hi, c.norm_hi, sizeof(a.norm_hi));
     return a;
@@ -303,7 +306,7 @@ uint32_t agft_struct_size(int which)
 size_t agft_workspace_bytes(const agft_config *cfg)
 {
     if (validate(cfg) != AGFT_OK) return 0;
-    return make_layout(cfg->n_tuners, cfg->d).total;
+    return make_layout(cfg->n_tuners, cfg->d, cfg->closed.enable == 2u).total;
 }
 
 agft_status agft_create(const agft_config *cfg, const agft_tuner_params *d_params, void *d_workspace,
@@ -315,7 +318,7 @@ agft_status agft_create(const agft_config *cfg, const agft_tuner_params *d_param
     if (st != AGFT_OK) return st;
     if (!d_params || !d_workspace) return AGFT_E_INVALID_ARG;
     if (reinterpret_cast<uintptr_t>(d_workspace) % 256 != 0) return AGFT_E_WORKSPACE;
-    const Layout L = make_layout(cfg->n_tuners, cfg->d);
+    const Layout L = make_layout(cfg->n_tuners, cfg->d, cfg->closed.enable == 2u);
     if (ws_bytes < L.total) return AGFT_E_WORKSPACE;
 
     int dev = 0, major = 0;
@@ -369,7 +372,7 @@ agft_status agft_attach(const agft_config *cfg, void *d_workspace, size_t ws_byt
     if (st != AGFT_OK) return st;
     if (!d_workspace) return AGFT_E_INVALID_ARG;
     if (reinterpret_cast<uintptr_t>(d_workspace) % 256 != 0) return AGFT_E_WORKSPACE;
-    const Layout L = make_layout(cfg->n_tuners, cfg->d);
+    const Layout L = make_layout(cfg->n_tuners, cfg->d, cfg->closed.enable == 2u);
     if (ws_bytes < L.total) return AGFT_E_WORKSPACE;
     int dev = 0, major = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return AGFT_E_DEVICE;
@@ -506,7 +509,8 @@ static agft_status run_steps(agft_handle h, const void *d_records, uint32_t t0, 
         cudaError_t e = cudaSuccess;
         // refinement re-admits arms, so a tuner's class can grow: without the deferred pass, one
         // warp per tuner throughout
-        if (c.kernel_policy == AGFT_POLICY_WIDE || (c.refine.enable && !defer)) {
+        // (ENV-S servers, closed.enable = 2, run on the WIDE mapping: a warp per tuner drives its server)
+        if (c.kernel_policy == AGFT_POLICY_WIDE || (c.refine.enable && !defer) || c.closed.enable == 2u) {
             e = prof_begin(h, kClsWide, h->stream, &a);
             if (e == cudaSuccess) e = launch_replay(a, c.d, h->stream);
             if (e == cudaSuccess) e = prof_end(h, h->stream);

@@ -20,6 +20,7 @@
 // MEASURED (E, TPOT, TTFT) at k* in place of ENV-R and runs a8–a11 exactly as the replay does.
 #include "env_t.cuh"
 #include "step_common.cuh"
+#include "des.cuh"
 
 namespace agft {
 
@@ -100,7 +101,8 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
     extern __shared__ double smem[];
     double *s_dec = smem, *s_pre = smem + kMaxArms, *s_pw = smem + 2 * kMaxArms;
     const EnvConsts *ec = a.w.env;
-    if (MODE == 0) {                                  // the live modes take no dynamic shared memory
+    constexpr bool kRep = MODE == 0 || MODE == 4;    // the replay (4: on the ENV-S server, ENV.md §7)
+    if (kRep) {                                       // the live modes take no dynamic shared memory
         for (int i = threadIdx.x; i < kMaxArms; i += blockDim.x) {
             s_dec[i] = ec->dec[i];
             s_pre[i] = ec->pre[i];
@@ -140,7 +142,7 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
     // ([slot][entry][lane]); a live window (MODE 1 / 2) reads and updates them in place in HBM
     // (arm index fastest: 32 consecutive arms = one coalesced 256-B row), with no dynamic shared
     // memory, so more tuners are in flight per SM.  Entry e of slot j: A[j * aJ + e * aS].
-    constexpr bool kInPlace = MODE != 0;
+    constexpr bool kInPlace = !kRep;
     constexpr int aS = kInPlace ? kMaxArms : 32, aJ = kInPlace ? 32 : P * 32, tJ = kInPlace ? 32 : D * 32;
     double *sA = kInPlace ? a.w.ainv + (size_t)tb * P * kMaxArms : smem + 3 * kMaxArms + (size_t)warp * S * (P + D) * 32;
     double *sT = kInPlace ? a.w.theta + (size_t)tb * D * kMaxArms : sA + S * P * 32;
@@ -160,7 +162,7 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
         const uint32_t k = 32u * j + lane;
         const bool on = k < K && ((a.w.active[tb * 4 + j] >> lane) & 1u);
         if (on) act |= 1u << j;
-        if (MODE == 0) {
+        if (kRep) {
 #pragma unroll
             for (int e = 0; e < P; ++e) sA[(j * P + e) * 32 + lane] = a.w.ainv[(tb * P + e) * kMaxArms + k];
 #pragma unroll
@@ -183,14 +185,22 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
     const uint32_t M = a.median_window;
 
     const StepRec *rp = a.records + (size_t)prm.trace_id * a.rec_stride + a.rec_off;
-    const uint32_t *rawp = (MODE == 0 && a.cl_enable) ? a.raw + ((size_t)prm.trace_id * a.rec_stride + a.rec_off) * AGFT_ROW_WORDS
+    const uint32_t *rawp = (kRep && a.cl_enable) ? a.raw + ((size_t)prm.trace_id * a.rec_stride + a.rec_off) * AGFT_ROW_WORDS
                                                       : nullptr;
     uint32_t clq = 0u, clqb = 0u;                     // ENV-C backlogs (ENV.md §6)
-    if (rawp) {
+    if (MODE == 0 && rawp) {
         clq = a.w.clq[tb * 2];
         clqb = a.w.clq[tb * 2 + 1];
     }
     double *bglob = a.w.b + tb * D * kMaxArms;
+    // ENV-S (ENV.md §7): the tuner's server, its Philox key (the trace's, §1) and queue
+    DesWarp des;
+    DesReq *desq = nullptr;
+    const Philox des_ph{(uint32_t)a.seed ^ (a.trace_base + prm.trace_id), (uint32_t)(a.seed >> 32)};
+    if constexpr (MODE == 4) {
+        des.load(a.w.des + tb, a.w.desr + tb * kDesR, lane);
+        desq = a.w.desq + tb * kDesQ;
+    }
 
     // ENV.md §4.11 mixed maturity-based refinement as of step t at context x (after pruning)
     auto refine = [&](uint32_t t, const double (&x)[D]) {
@@ -265,7 +275,13 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
         double x[D];
         double g = 0.0, invIm = 0.0, invAm = 0.0, wIm = 0.0, nT = 0.0, nE = 0.0, baseE = 0.0, baseEDP = 0.0;
         uint32_t recI = 0u, recP = 0u, arr_cl = 0u;
-        if constexpr (MODE == 0 || MODE == 3) {
+        if constexpr (MODE == 4) {                    // ENV-S: the snapshot of the last window (§7)
+            double xr[7];
+            context_of(des.snap[0], des.snap[1], des.snap[2], des.snap[3], des.snap[4], des.snap[5], des.snap[6],
+                       des.snap[7], a.W, a.kv_total, a.norm_lo, a.norm_hi, xr);
+#pragma unroll
+            for (int i = 0; i < D; ++i) x[i] = xr[i];
+        } else if constexpr (MODE == 0 || MODE == 3) {
             const StepRec &rec = rp[s];
             if (s + 1 < a.n_steps && lane == 0) {
                 prefetch_l1(&rp[s + 1]);
@@ -406,6 +422,13 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
                 st.flags |= 1u;
                 break;
             }
+        } else if constexpr (MODE == 4) {             // ENV-S: the window on the tuner's own server
+            const DesOut o = des.window(t, rawp + (size_t)s * AGFT_ROW_WORDS, a.tc, des_ph, desq, s_dec[kstar],
+                                        s_pre[kstar], s_pw[kstar], a, lane);
+            E = o.E;
+            tpot = o.tpot;
+            ttft = o.ttft;
+            edp = o.edp;
         } else {
         const double dec = s_dec[kstar], pre = s_pre[kstar], pw = s_pw[kstar];
         const double t_dec = xmul((double)recI, dec);
@@ -641,13 +664,13 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
 #pragma unroll
     for (int j = 0; j < S; ++j) {
         const uint32_t k = 32u * j + lane;
-        if (MODE == 0) {
+        if (kRep) {
 #pragma unroll
             for (int e = 0; e < P; ++e) a.w.ainv[(tb * P + e) * kMaxArms + k] = sA[(j * P + e) * 32 + lane];
 #pragma unroll
             for (int i = 0; i < D; ++i) a.w.theta[(tb * D + i) * kMaxArms + k] = sT[(j * D + i) * 32 + lane];
         }
-        if (MODE == 0 || k == kpend) {                // a live window changed only the chosen arm's counters
+        if (kRep || k == kpend) {                // a live window changed only the chosen arm's counters
             a.w.n[tb * kMaxArms + k] = n[j];
             a.w.rbar[tb * kMaxArms + k] = rbar[j];
             a.w.ebar[tb * kMaxArms + k] = ebar[j];
@@ -655,7 +678,8 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
         const uint32_t bits = __ballot_sync(kFull, (act >> j) & 1u);
         if (lane == 0) a.w.active[tb * 4 + j] = bits;
     }
-    if (rawp && lane == 0) {
+    if constexpr (MODE == 4) des.save(a.w.des + tb, a.w.desr + tb * kDesR, lane);
+    if (MODE == 0 && rawp && lane == 0) {
         a.w.clq[tb * 2] = clq;
         a.w.clq[tb * 2 + 1] = clqb;
     }
@@ -694,7 +718,7 @@ template <int D, int S, int MODE>
 static cudaError_t launch_ds(const ReplayArgs &a, cudaStream_t s)
 {
     constexpr int P = D * (D + 1) / 2;
-    const size_t smem = MODE == 0 ? (3 * kMaxArms + (size_t)kWarpsPerBlock * S * (P + D) * 32) * sizeof(double) : 0;
+    const size_t smem = (MODE == 0 || MODE == 4) ? (3 * kMaxArms + (size_t)kWarpsPerBlock * S * (P + D) * 32) * sizeof(double) : 0;
     auto kern = replay_kernel<D, S, MODE>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -730,7 +754,10 @@ static cudaError_t launch_mode(const ReplayArgs &a, uint32_t D, cudaStream_t s)
     }
 }
 
-cudaError_t launch_replay(const ReplayArgs &a, uint32_t D, cudaStream_t s) { return launch_mode<0>(a, D, s); }
+cudaError_t launch_replay(const ReplayArgs &a, uint32_t D, cudaStream_t s)
+{
+    return a.cl_enable == 2u ? launch_mode<4>(a, D, s) : launch_mode<0>(a, D, s);   // ENV-S (ENV.md §7)
+}
 
 cudaError_t launch_live(const ReplayArgs &a, uint32_t D, int mode, cudaStream_t s)
 {

@@ -101,7 +101,7 @@ cudaError_t launch_trace(const TraceArgs &a, cudaStream_t s)
 // ---------------------------------------------------------------- workspace init
 struct InitArgs {
     Ws w;
-    uint32_t N, K, D;
+    uint32_t N, K, D, des;
     uint32_t f_min_mhz, f_step_mhz, f_max_hw_mhz;
     agft_env env;
 };
@@ -168,6 +168,14 @@ __global__ void init_tuner_kernel(const __grid_constant__ InitArgs a)
             a.w.wmeta[tb * 2 + k] = 0;
             a.w.clq[tb * 2 + k] = 0;                    // ENV-C: no backlog at t = 0 (ENV.md §6)
         }
+        if (a.des && k < (uint32_t)kDesR) {            // ENV-S (ENV.md §7): idle server, empty slots
+            DesSlot sl = {};
+            a.w.desr[tb * kDesR + k] = sl;
+            if (k == 0) {
+                DesScal sc = {};
+                a.w.des[tb] = sc;
+            }
+        }
         if (k == 0) {
             agft_tuner_stats st = {};
             st.traj_hash = kFnvOffset;
@@ -189,6 +197,7 @@ cudaError_t launch_init(const Ws &w, const agft_config &cfg, cudaStream_t s)
     a.N = cfg.n_tuners;
     a.K = cfg.grid.n_arms;
     a.D = cfg.d;
+    a.des = cfg.closed.enable == 2u ? 1u : 0u;
     a.f_min_mhz = cfg.grid.f_min_mhz;
     a.f_step_mhz = cfg.grid.f_step_mhz;
     a.f_max_hw_mhz = cfg.grid.f_max_hw_mhz;

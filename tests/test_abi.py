@@ -137,10 +137,16 @@ def test_record_slot_count():
 
 
 def test_closed_loop_and_attach_host_checks(lib):
-    """ABI v5: agft_closed validation, and agft_attach's host-side checks (no kernel launched)."""
+    """ABI v5/v8: agft_closed validation (1 ENV-C, 2 ENV-S, nothing else), the ENV-S workspace, and
+    agft_attach's host-side checks (no kernel launched)."""
     import ctypes
     import numpy as np
-    assert _bad(lib, cl_enable=2) == -1
+    assert _bad(lib, cl_enable=3) == -1
+    assert _bad(lib, cl_enable=2) == 0
+    c1 = _abi.make_config(dict(named_config("C2"), n_tuners=10), n_tuners=10)
+    c2 = _abi.make_config(dict(named_config("C2"), n_tuners=10, cl_enable=2), n_tuners=10)
+    # ENV-S adds the server of every tuner: 128-B scalars + 512 queued + 128 running requests of 24 B
+    assert pkg.agft_workspace_bytes(c2) - pkg.agft_workspace_bytes(c1) >= 10 * (128 + 640 * 24)
     assert _bad(lib, cl_enable=1, cl_q_max=0) == 0            # a zero cap is the open loop (ENV.md §6)
     c = _abi.make_config(named_config("C2"))
     h = ctypes.c_void_p()

@@ -108,16 +108,19 @@ struct DesWarp {
         }
         __syncwarp();                                         // the queue writes before the head reads
 
-        // ---- the engine (ENV.md §7), warp-uniform control
+        // ---- the engine (ENV.md §7), warp-uniform control; the queue head is kept in registers
         const double t_end = xmul((double)(t + 1u), a.W);
+        DesReq h;
+        if (qlen > 0u) h = q[qhead];
         uint32_t P = 0, Dc = 0, I = 0, hits = 0, misses = 0, n_tok = 0, n_first = 0;
         double busy = 0.0, sdec = 0.0, sfirst = 0.0;
+        uint32_t g_n = 0xFFFFFFFFu;                          // running count the penalty g was computed for
+        double g = 1.0;
         while (clock < t_end) {
             uint32_t npre = 0, fresh[kDesS];
 #pragma unroll
             for (int j = 0; j < kDesS; ++j) fresh[j] = 0u;
             while (qlen > 0u) {                               // admission: FIFO, head of line
-                const DesReq h = q[qhead];
                 if (!(h.arr <= clock) || nrun >= (uint32_t)kDesR || (uint64_t)kv + h.ctx + h.gen > a.kv_total) break;
                 const uint32_t wd = h.tmpl >> 5, bit = 1u << (h.tmpl & 31u);
                 const uint32_t hit = (__shfl_sync(kFull, store, (int)wd) & bit) ? 1u : 0u;
@@ -126,40 +129,44 @@ struct DesWarp {
                 misses += 1u - hit;
                 npre += h.ctx - (hit ? h.ctx / 2u : 0u);
                 kv += h.ctx + h.gen;
+                {                                             // the lowest free slot (j-major, then lane)
+                    static_assert(kDesS == 4, "four slots per lane");
+                    const uint32_t fm0 = __ballot_sync(kFull, !(flags[0] & 1u)), fm1 = __ballot_sync(kFull, !(flags[1] & 1u)),
+                                   fm2 = __ballot_sync(kFull, !(flags[2] & 1u)), fm3 = __ballot_sync(kFull, !(flags[3] & 1u));
+                    const int js = fm0 ? 0 : fm1 ? 1 : fm2 ? 2 : 3;
+                    const uint32_t fm = fm0 ? fm0 : fm1 ? fm1 : fm2 ? fm2 : fm3;
+                    const int owner = __ffs(fm) - 1;
 #pragma unroll
-                for (int j = 0; j < kDesS; ++j) {             // the lowest free slot
-                    const uint32_t fm = __ballot_sync(kFull, !(flags[j] & 1u));
-                    if (fm) {
-                        const int owner = __ffs(fm) - 1;
-                        if (lane == owner) {
+                    for (int j = 0; j < kDesS; ++j) {          // (no early exit: the slots stay in registers)
+                        if (j == js && lane == owner) {
                             arr[j] = h.arr;
                             ctx[j] = h.ctx;
                             gen[j] = h.gen;
                             done[j] = 0u;
                             flags[j] = 1u;
                         }
-                        fresh[j] |= 1u << owner;
-                        break;
+                        if (j == js) fresh[j] |= 1u << owner;
                     }
                 }
                 nrun += 1u;
                 qhead = (qhead + 1u) % (uint32_t)kDesQ;
                 qlen -= 1u;
+                if (qlen > 0u) h = q[qhead];
             }
             uint32_t ndec = 0;
 #pragma unroll
             for (int j = 0; j < kDesS; ++j) ndec += (uint32_t)__popc(__ballot_sync(kFull, (flags[j] & 3u) == 3u));
             if (npre == 0u && ndec == 0u) {                   // idle until the next arrival
                 double nxt = t_end;
-                if (qlen > 0u) {
-                    const double ha = q[qhead].arr;
-                    if (ha < t_end) nxt = ha;
-                }
+                if (qlen > 0u && h.arr < t_end) nxt = h.arr;
                 clock = nxt;
                 continue;
             }
-            const double rho = xdiv((double)nrun, (double)a.cap);
-            const double g = rho > 1.0 ? xmul(rho, xsqrt(rho)) : 1.0;
+            if (nrun != g_n) {                                // the penalty changes only with nrun
+                const double rho = xdiv((double)nrun, (double)a.cap);
+                g = rho > 1.0 ? xmul(rho, xsqrt(rho)) : 1.0;
+                g_n = nrun;
+            }
             const double tp = xmul((double)npre, pre), td = ndec > 0u ? dec : 0.0;
             const double dt = xadd(kDesOver, xmul(tp > td ? tp : td, g));
             clock = xadd(clock, dt);

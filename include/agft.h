@@ -341,6 +341,10 @@ typedef struct {
     uint32_t launches[8];
 } agft_profile;
 agft_status agft_profile_start(agft_handle h, int serialize);
+/* Resident tuners per SM of replay class `slot` (0..5 as above) for cfg's d and grid, from the CUDA
+ * occupancy calculator (registers, shared memory, block size): the residency term of the latency
+ * roofline (resident tuners ÷ chain latency per window).  Needs the device; no kernel launched. */
+agft_status agft_occupancy(const agft_config *cfg, int slot, uint32_t *tuners_per_sm);
 agft_status agft_profile_read(agft_handle h, agft_profile *out);
 
 /* Frees the host handle only; the caller frees its device buffers. */

@@ -149,6 +149,13 @@ def agft_profile_read(h) -> dict:
             for i, name in enumerate(_abi.PROFILE_SLOTS)}
 
 
+def agft_occupancy(cfg_c, slot: int) -> int:
+    """Resident tuners per SM of replay class `slot` (_abi.PROFILE_SLOTS order) for this config."""
+    v = C.c_uint32()
+    _abi.check("agft_occupancy", _abi.lib().agft_occupancy(C.byref(cfg_c), slot, C.byref(v)))
+    return v.value
+
+
 def agft_sweep(h, records, t0, n_steps, S, SP, NP, O, best=None):
     _abi.check("agft_sweep", _abi.lib().agft_sweep(h, _p(records), t0, n_steps, _p(S), _p(SP), _p(NP), _p(O),
                                                     _p(best)))

@@ -120,6 +120,7 @@ PROTOTYPES = {
     "agft_kernel_launches": (C.c_uint64, []),
     "agft_profile_start": (C.c_int, [vp, C.c_int]),
     "agft_profile_read": (C.c_int, [vp, vp]),
+    "agft_occupancy": (C.c_int, [C.POINTER(AgftConfig), C.c_int, C.POINTER(u32)]),
 }
 
 # agft_profile slots (include/agft.h): the replay classes, then the classification and refinement passes

@@ -744,6 +744,32 @@ agft_status agft_destroy(agft_handle h)
     return AGFT_OK;
 }
 
+agft_status agft_occupancy(const agft_config *cfg, int slot, uint32_t *tuners_per_sm)
+{
+    if (!tuners_per_sm || slot < 0 || slot > 5) return AGFT_E_INVALID_ARG;
+    agft_status st = validate(cfg);
+    if (st != AGFT_OK) return st;
+    int dev = 0, major = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess || major != 10)
+        return AGFT_E_DEVICE;
+    int v = -1;
+    switch (slot) {
+    case kClsWide: v = occupancy_wide(cfg->d, cfg->grid.n_arms); break;
+    case kClsSeg32: v = occupancy_seg2(cfg->d, 16); break;
+    case kClsSeg16: v = occupancy_seg2(cfg->d, 8); break;
+    case kClsSeg8: v = occupancy_seg2(cfg->d, 4); break;
+    case kClsSeg64: v = occupancy_seg2(cfg->d, 32); break;
+    default: v = occupancy_solo(cfg->d); break;
+    }
+    if (v < 0) {
+        cudaGetLastError();
+        return AGFT_E_CUDA;
+    }
+    *tuners_per_sm = (uint32_t)v;
+    return AGFT_OK;
+}
+
 agft_status agft_profile_start(agft_handle h, int serialize)
 {
     if (!h || serialize < 0 || serialize > 1) return AGFT_E_INVALID_ARG;

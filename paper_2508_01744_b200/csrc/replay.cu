@@ -727,6 +727,43 @@ static cudaError_t launch_ds(const ReplayArgs &a, cudaStream_t s)
     return cudaGetLastError();
 }
 
+template <int D, int S>
+static int occupancy_ds()
+{
+    constexpr int P = D * (D + 1) / 2;
+    const size_t smem = (3 * kMaxArms + (size_t)kWarpsPerBlock * S * (P + D) * 32) * sizeof(double);
+    auto kern = replay_kernel<D, S, 0>;
+    int blocks = 0;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, kWarpsPerBlock * 32, smem) != cudaSuccess)
+        return -1;
+    return blocks * kWarpsPerBlock;                   // one tuner per warp
+}
+
+template <int D>
+static int occupancy_d(uint32_t K)
+{
+    switch ((K + 31) / 32) {
+    case 1: return occupancy_ds<D, 1>();
+    case 2: return occupancy_ds<D, 2>();
+    case 3: return occupancy_ds<D, 3>();
+    default: return occupancy_ds<D, 4>();
+    }
+}
+
+int occupancy_wide(uint32_t D, uint32_t K)
+{
+    switch (D) {
+    case 1: return occupancy_d<1>(K);
+    case 2: return occupancy_d<2>(K);
+    case 3: return occupancy_d<3>(K);
+    case 4: return occupancy_d<4>(K);
+    case 5: return occupancy_d<5>(K);
+    case 6: return occupancy_d<6>(K);
+    default: return occupancy_d<7>(K);
+    }
+}
+
 template <int D, int MODE>
 static cudaError_t launch_d(const ReplayArgs &a, cudaStream_t s)
 {

@@ -513,6 +513,43 @@ static cudaError_t launch_seg2_dg(const ReplayArgs &a, cudaStream_t s)
     return cudaGetLastError();
 }
 
+template <int D, int G>
+static int occupancy_seg2_dg()
+{
+    constexpr int P = D * (D + 1) / 2;
+    const size_t smem = seg2_smem_bytes<G>(P, D);
+    auto kern = seg2_kernel<D, G>;
+    int blocks = 0;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, kSeg2Warps * 32, smem) != cudaSuccess)
+        return -1;
+    return blocks * kSeg2Warps * (32 / G);
+}
+
+template <int D>
+static int occupancy_seg2_d(int G)
+{
+    switch (G) {
+    case 4: return occupancy_seg2_dg<D, 4>();
+    case 32: return occupancy_seg2_dg<D, 32>();
+    case 8: return occupancy_seg2_dg<D, 8>();
+    default: return occupancy_seg2_dg<D, 16>();
+    }
+}
+
+int occupancy_seg2(uint32_t D, int G)
+{
+    switch (D) {
+    case 1: return occupancy_seg2_d<1>(G);
+    case 2: return occupancy_seg2_d<2>(G);
+    case 3: return occupancy_seg2_d<3>(G);
+    case 4: return occupancy_seg2_d<4>(G);
+    case 5: return occupancy_seg2_d<5>(G);
+    case 6: return occupancy_seg2_d<6>(G);
+    default: return occupancy_seg2_d<7>(G);
+    }
+}
+
 template <int D>
 static cudaError_t launch_seg2_d(const ReplayArgs &a, int G, cudaStream_t s)
 {

@@ -166,6 +166,27 @@ static cudaError_t launch_solo_d(const ReplayArgs &a, cudaStream_t s)
     return cudaGetLastError();
 }
 
+template <int D>
+static int occupancy_solo_d()
+{
+    int blocks = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, solo_kernel<D>, kSoloThreads, 0) != cudaSuccess) return -1;
+    return blocks * kSoloThreads;                     // one tuner per lane
+}
+
+int occupancy_solo(uint32_t D)
+{
+    switch (D) {
+    case 1: return occupancy_solo_d<1>();
+    case 2: return occupancy_solo_d<2>();
+    case 3: return occupancy_solo_d<3>();
+    case 4: return occupancy_solo_d<4>();
+    case 5: return occupancy_solo_d<5>();
+    case 6: return occupancy_solo_d<6>();
+    default: return occupancy_solo_d<7>();
+    }
+}
+
 cudaError_t launch_solo(const ReplayArgs &a, uint32_t D, cudaStream_t s)
 {
     if (a.n_tuners == 0 || a.n_steps == 0) return cudaSuccess;

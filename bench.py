@@ -69,6 +69,23 @@ def profile_traffic(workload_key: str):
     return None
 
 
+def latency_roofline():
+    """Per-class latency ceilings (resident tuners ÷ chain latency per window) measured for THIS build by
+    tools/latency_roofline.py (profiles/*latency_roofline.json, matched on the source hash), or None."""
+    import glob
+    sha = src_sha()
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*latency_roofline.json")), reverse=True):
+        try:
+            with open(path) as f:
+                lr = json.load(f)
+        except (OSError, ValueError):
+            continue
+        if lr.get("src_sha") == sha:
+            lr["source"] = os.path.relpath(path, ROOT)
+            return lr
+    return None
+
+
 def measured_fp64_peak():
     """FP64 DFMA TFLOP/s measured on a B200 of this pool by tools/fp64_peak.cu (profiles/*fp64_peak.json)."""
     import glob
@@ -223,6 +240,7 @@ def class_roofline(d, prof, prof_conc, steps, replay_ms, serial_replay_ms, st, n
     sm_mhz = float(pk.get("sm_max_mhz", 1965.0))
     peak_fp64 = N_SM * FP64_UNITS_PER_SM * 2 * sm_mhz * 1e6 / 1e12
     meas, meas_src = measured_fp64_peak()
+    lat = latency_roofline()
     classes = {}
     for name, c in prof.items():
         if not c["launches"]:
@@ -237,6 +255,10 @@ def class_roofline(d, prof, prof_conc, steps, replay_ms, serial_replay_ms, st, n
                       "tuner_steps": c["tuner_steps"], "mean_active_arms": round(c["active_arm_steps"] / c["tuner_steps"], 3),
                       "tuner_steps_per_s": round(c["tuner_steps"] / (c["kernel_ms"] / 1e3), 1),
                       "achieved_tflops": round(ach, 4), "frac": round(ach / peak_fp64, 5)})
+        if lat and name in lat.get("classes", {}) and "tuner_steps_per_s" in e:
+            ceil = lat["classes"][name]["latency_ceiling_tuner_steps_per_s"]
+            e["latency_ceiling_tuner_steps_per_s"] = ceil
+            e["frac_of_latency_ceiling"] = round(e["tuner_steps_per_s"] / ceil, 4)
         if traffic and name in traffic.get("classes", {}):
             tc = traffic["classes"][name]
             e["traffic_per_launch"] = tc["dram_bytes"] / max(1, tc["launches"])
@@ -260,6 +282,9 @@ def class_roofline(d, prof, prof_conc, steps, replay_ms, serial_replay_ms, st, n
                                  "frac": round(step_flops / (replay_ms / 1e3) / 1e12 / peak_fp64, 5),
                                  "replay_ms": round(replay_ms, 3), "mean_active_arms": round(sum_active / (float(n) * T), 3)},
                 "classes": classes,
+                "latency_roofline": ({"source": lat["source"], "bound": "latency: resident tuners ÷ chain latency per "
+                                      "window, per class at its full K (tools/latency_roofline.py)"}
+                                     if lat else None),
                 "traffic_source": traffic.get("source") if traffic else None,
                 "traffic_total_bytes_per_step": traffic.get("total_dram_bytes") if traffic else None,
                 # records once (128 B per window and trace) + the stats

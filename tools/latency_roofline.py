@@ -98,7 +98,8 @@ def main():
                       "full_wave_frac_of_ceiling": round(full_rate / ceiling, 4),
                       "sm_mhz": clk}
         print(name, json.dumps(rows[name]), flush=True)
-    out = {"how": "tools/latency_roofline.py: one warp of tuners alone (chain latency) and one full wave "
+    import bench
+    out = {"src_sha": bench.src_sha(), "how": "tools/latency_roofline.py: one warp of tuners alone (chain latency) and one full wave "
                   "(agft_occupancy × 148 SMs) of a class pinned by K with pruning never firing; "
                   f"T = {args.T} windows, best of 3 replays, CUDA events", "classes": rows,
            "when": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime())}

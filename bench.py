@@ -160,23 +160,38 @@ def peaks() -> dict:
     return {}
 
 
-def run_cpu_baseline(cfg: dict, n_tuners: int, T: int) -> dict:
+def parity_sample(cfg: dict, n: int, k: int = 256) -> list:
+    """The tuners the cpu_baseline leg replays through the oracle: for the α × pruning sweep, every
+    4th hyper-parameter point of four traces spread over the shard (diurnal and burst patterns),
+    else the first k tuners."""
+    if cfg.get("sweep") == "hyper256" and n >= 1024 and n % 256 == 0:
+        R = n // 256
+        traces = sorted({0, R // 3, (2 * R) // 3, R - 1}) if R >= 4 else list(range(R))
+        per = k // len(traces)
+        step = max(1, 256 // per)
+        return [r * 256 + h for r in traces for h in range(0, 256, step)][:k]
+    return list(range(min(k, n)))
+
+
+def run_cpu_baseline(cfg: dict, ids: list, T: int) -> dict:
     """The oracle as it stands on this host's cores, on a bounded sample of the workload."""
     import oracle
     from agft_inputs import tuner_params
-    params = tuner_params(cfg, list(range(n_tuners)))
+    n_tuners = len(ids)
+    params = tuner_params(cfg, list(ids))
     cores = os.cpu_count() or 1
     t = time.perf_counter()
     ost = oracle.run_batch(cfg, params, T, threads=cores)
     dt = time.perf_counter() - t
     n1 = min(4, n_tuners)                              # SURVEY §8(d): the 1-thread rate beside it
     t1 = time.perf_counter()
-    oracle.run_batch(cfg, tuner_params(cfg, list(range(n1))), T, threads=1)
+    oracle.run_batch(cfg, tuner_params(cfg, list(ids[:n1])), T, threads=1)
     dt1 = time.perf_counter() - t1
     return {"value": n_tuners * T / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "one_thread_value": n1 * T / dt1, "one_thread_sample": f"tuners 0..{n1 - 1} × {T} steps, 1 thread",
-            "sample": f"{cfg.get('name', 'C4')} tuners 0..{n_tuners - 1}"
-                      f"{' (trace 0, all 256 hyper-parameter points)' if cfg.get('sweep') == 'hyper256' else ''} × {T} steps, "
+            "one_thread_value": n1 * T / dt1, "one_thread_sample": f"{n1} tuners × {T} steps, 1 thread",
+            "sample": f"{cfg.get('name', 'C4')}: {n_tuners} tuners (traces "
+                      f"{sorted({int(t) for t in params['trace_id']})}, "
+                      f"{len(set(int(i) % 256 for i in ids))} hyper-parameter points each) × {T} steps, "
                       f"free-running, {dt:.1f} s on {cores} threads"}, ost
 
 
@@ -210,16 +225,17 @@ def arm_state_errors(cfg, params, tb, T, sample) -> dict:
             "arm_counters_b_exact": exact, "arm_state_tolerance": 1e-9}
 
 
-def parity_summary(gst, ost) -> dict:
+def parity_summary(gst, ost, ids=None) -> dict:
     """The timed run's own statistics for the tuners the cpu_baseline leg ran through the oracle
     (same config, same windows): trajectory-hash matches and, for those, exact equality of every
     counter and fp64 sum (ENV.md §0).  A free-running oracle may leave the GPU's path at a near-tie
     (ENV.md §4.5); the GPU's near-tie count is reported beside it."""
-    n = min(len(ost), len(gst))
-    match = [i for i in range(n) if int(gst["traj_hash"][i]) == ost[i]["traj_hash"]]
-    exact = [i for i in match if all(gst[f][i] == ost[i][f] for f in PARITY_EXACT)]
+    ids = list(range(min(len(ost), len(gst)))) if ids is None else list(ids)
+    n = len(ids)
+    match = [j for j, i in enumerate(ids) if int(gst["traj_hash"][i]) == ost[j]["traj_hash"]]
+    exact = [j for j in match if all(gst[f][ids[j]] == ost[j][f] for f in PARITY_EXACT)]
     return {"tuners": n, "traj_hash_match": len(match), "stats_exact_given_traj": len(exact),
-            "near_tie_steps_gpu": int(gst["near_tie_steps"][:n].astype(np.int64).sum()),
+            "near_tie_steps_gpu": int(gst["near_tie_steps"][ids].astype(np.int64).sum()),
             "fields": list(PARITY_EXACT),
             "oracle": "free-running fp64 C oracle of the cpu_baseline leg, same config and windows"}
 
@@ -471,9 +487,10 @@ def main():
     if not args.no_e2e:
         out["e2e"] = e2e_leg(cfg, params, sh.trace_base, world, local, chunk, n, T, args)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"], ost = run_cpu_baseline(cfg, min(256, n), T)
-        out["parity"] = parity_summary(st, ost)
-        out["parity"].update(arm_state_errors(cfg, params, tb, T, [i for i in (0, 63, 128, 255) if i < n]))
+        ids = parity_sample(cfg, n)
+        out["cpu_baseline"], ost = run_cpu_baseline(cfg, ids, T)
+        out["parity"] = parity_summary(st, ost, ids)
+        out["parity"].update(arm_state_errors(cfg, params, tb, T, [ids[j] for j in (0, 63, 128, 255) if j < len(ids)]))
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:

@@ -24,6 +24,7 @@ def main(T: int):
         "refine_classes": (dict(c4, ph_enable=0, rf_enable=1), 0),
         "phase_refine_wide": (dict(c4, ph_enable=1, rf_enable=1), 0),
         "closed": (dict(c4, cl_enable=1), 0),
+        "des": (dict(c4, cl_enable=2, n_tuners=64), 0),
         "C1": (named_config("C1"), 0),
     }
     for name, (cfg, pol) in cases.items():

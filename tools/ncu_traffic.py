@@ -2,7 +2,9 @@
 --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum, written as the
 profiles/*_traffic.json that bench.py matches on (source hash, workload key).
 
-usage: ncu_traffic.py LAUNCHES_CSV OUT_JSON WORKLOAD_KEY"""
+usage: ncu_traffic.py LAUNCHES_CSV OUT_JSON WORKLOAD_KEY [DAYS]
+(DAYS = replay days in the capture: `bench.py --steps 1 --warmup 0` replays the timed day and the
+serialised attribution day, so 2)"""
 import csv
 import json
 import os
@@ -34,7 +36,7 @@ def slot(name: str) -> str:
     return "other"
 
 
-def main(path, out, key):
+def main(path, out, key, days="2"):
     rows = list(csv.reader(open(path)))
     hdr = None
     per = defaultdict(lambda: defaultdict(float))
@@ -54,11 +56,12 @@ def main(path, out, key):
         c["dram_bytes"] += m.get("dram__bytes_read.sum", 0.0) + m.get("dram__bytes_write.sum", 0.0)
         c["ncu_ms"] += m.get("gpu__time_duration.sum", 0.0)
     tot = sum(c["dram_bytes"] for k, c in classes.items() if k not in ("trace", "other"))
-    json.dump({"src_sha": bench.src_sha(), "workload_key": key, "classes": classes, "total_dram_bytes": tot,
+    json.dump({"src_sha": bench.src_sha(), "workload_key": key, "classes": classes, "days_in_capture": int(days),
+               "total_dram_bytes": tot / int(days),
                "how": "ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
                       "--clock-control none over every launch of one bench step (cold, serialised)"},
               open(out, "w"), indent=1)
 
 
 if __name__ == "__main__":
-    main(*sys.argv[1:4])
+    main(*sys.argv[1:5])

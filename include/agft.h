@@ -16,7 +16,9 @@
  *    error is sticky on the handle (every later call returns AGFT_E_CUDA).
  *  - A handle is not thread-safe (single writer).
  *  - Device-side anomalies never abort: a non-finite EDP or reward sets bit 0 of
- *    the tuner's stats.flags and freezes that tuner.
+ *    the tuner's stats.flags and freezes that tuner; an update that leaves A⁻¹ not positive
+ *    definite (xᵀA⁻¹x < 0, or a diagonal entry ≤ 0: a corrupted or numerically broken arm; SPEC
+ *    S:207) sets bits 0 and 1 and freezes it (the step that detects it may still be counted).
  *  - Layout and arithmetic of every step follow ENV.md (the contract shared with
  *    the CPU oracle, which is a separate implementation).
  */

@@ -125,6 +125,9 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
         return;
     }
     __shared__ PhState s_ph[kWarpsPerBlock];          // ENV.md §4.10 detector (lane 0 owns it)
+    __shared__ uint32_t s_spd[kWarpsPerBlock];        // set by the owner lane on an SPD violation
+    if (lane == 0) s_spd[warp] = 0u;
+    __syncwarp();
     uint32_t phase = 0u;
     uint32_t extb = 0u;                               // bit j: arm 32j+lane was Extreme-pruned (ENV.md §4.11)
     if (a.rf_enable) {
@@ -272,6 +275,10 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
 
     for (uint32_t s = 0; s < a.n_steps; ++s) {
         const uint32_t t = a.t0 + s;
+        if (s_spd[warp]) {                                // the last step's update broke A⁻¹'s SPD property
+            st.flags |= kFlagFrozen | kFlagSpd;
+            break;
+        }
         double x[D];
         double g = 0.0, invIm = 0.0, invAm = 0.0, wIm = 0.0, nT = 0.0, nE = 0.0, baseE = 0.0, baseEDP = 0.0;
         uint32_t recI = 0u, recP = 0u, arr_cl = 0u;
@@ -487,6 +494,7 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
         }
 
         // ---- a9: rank-1 update of the chosen arm (Eqs. 3–5) by its owner lane
+        bool spd = true;
         if (lane == own) {
             double *Aj = sA + jst * aJ + lane;
             double *Tj = sT + jst * tJ + lane;
@@ -518,7 +526,12 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
 #pragma unroll
                 for (int r0 = 0; r0 < D; ++r0)
 #pragma unroll
-                    for (int c = r0; c < D; ++c, ++e) Aj[e * aS] = fma(-z[r0] * invd, z[c], Ap[e]);
+                    for (int c = r0; c < D; ++c, ++e) {
+                        const double v = fma(-z[r0] * invd, z[c], Ap[e]);
+                        Aj[e * aS] = v;
+                        if (c == r0) spd = spd && v > 0.0;
+                    }
+                spd = spd && spd_quad_ok(xz);
             }
             const double coef = (r - px) * invd;                // RLS form of θ = A⁻¹ b (AMB-21)
 #pragma unroll
@@ -533,6 +546,7 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
             put<S>(rbar, jst, xadd(pick<S>(rbar, jst), xmul(xsub(r, pick<S>(rbar, jst)), inv)));
             put<S>(ebar, jst, xadd(pick<S>(ebar, jst), xmul(xsub(edp, pick<S>(ebar, jst)), inv)));
         }
+        if (!spd) s_spd[warp] = 1u;                       // SPD guard: frozen from the next step
 
         // ---- a10: §4.3 pruning on the post-update state
         if (a.prune_enable) {

@@ -187,6 +187,7 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
 
     for (uint32_t s = 0; s < a.n_steps; ++s) {
         const uint32_t t = a.t0 + s;
+        live = live && !(st.flags & kFlagSpd);                        // an SPD violation last step froze it
 #if AGFT_TMA
         const StepRec *rc = rt.on ? rt.at(s, lane) : rp + s;
 #define RF(f) (rt.on ? rc->f : __ldg(&rc->f))
@@ -333,12 +334,13 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
         }
 
         // ---- a9: Sherman–Morrison on the owner lane's slot
+        bool spd = true;
         if (live && is_own) {
             double thv[D];
 #pragma unroll
             for (int i = 0; i < D; ++i) thv[i] = oslot ? th1[i] : th0[i];
-            if (kBS) sm_update_smem<D>(oslot ? A1 : A0, 32, thv, oslot ? B1 : B0, 32, x, r);
-            else sm_update_smem<D>(oslot ? A1 : A0, 32, thv, bg + kstar, kMaxArms, x, r);
+            if (kBS) spd = sm_update_smem<D>(oslot ? A1 : A0, 32, thv, oslot ? B1 : B0, 32, x, r);
+            else spd = sm_update_smem<D>(oslot ? A1 : A0, 32, thv, bg + kstar, kMaxArms, x, r);
 #pragma unroll
             for (int i = 0; i < D; ++i) {
                 if (oslot) th1[i] = thv[i]; else th0[i] = thv[i];
@@ -346,6 +348,7 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
             if (oslot) welford_inv(n1, rb1, eb1, r, o.edp, inv_n);
             else welford_inv(n0, rb0, eb0, r, o.edp, inv_n);
         }
+        if (!spd) atomicOr(&st.flags, kFlagFrozen | kFlagSpd);      // SPD guard: frozen from the next step
 
         // ---- a10: pruning (ENV.md §4.8)
         if (a.prune_enable) {

@@ -120,7 +120,10 @@ __global__ void __launch_bounds__(kSoloThreads, kSoloMinBlocks) solo_kernel(cons
 #pragma unroll
         for (int q = 0; q < D; ++q) x[q] = __ldg(&rc->x[q]);
         x[0] = x0;
-        sm_update<D>(A, th, b, x, r);
+        if (!sm_update<D>(A, th, b, x, r)) {                    // SPD guard: freeze (flags bit 1)
+            st.flags |= kFlagFrozen | kFlagSpd;
+            break;
+        }
         welford_inv(n, rbar, ebar, r, o.edp, inv_n);
         // a11
         stats_add(st, o, r, baseE, baseEDP, k, 1u);

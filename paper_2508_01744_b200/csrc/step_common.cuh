@@ -206,10 +206,18 @@ __device__ __forceinline__ constexpr int pidx(int r, int c)
     return r * D - r * (r - 1) / 2 + (c - r);
 }
 
+// SPD guard of a rank-1 update (SURVEY §5 failure detection; A⁻¹ stays symmetric
+// positive definite with eigenvalues in (0, 1] since λ_min(A) ≥ 1): xᵀA⁻¹x must not be negative
+// beyond rounding and every updated diagonal entry must stay positive.  A violation (a corrupted
+// or numerically broken arm) freezes the tuner with flags bit 1 (kFlagSpd).
+constexpr uint32_t kFlagFrozen = 1u, kFlagSpd = 2u;
+__device__ __forceinline__ bool spd_quad_ok(double xz) { return xz > -1e-12; }
+
 // Sherman–Morrison update of one arm held in registers (Eqs. 3–5, AMB-21):
 // z = A⁻¹x, δ = 1 + xᵀz, A⁻¹ ← A⁻¹ − z zᵀ/δ, θ ← θ + z (r − θ·x)/δ, b ← b + r x (exact).
+// Returns the SPD guard.
 template <int D>
-__device__ __forceinline__ void sm_update(double (&A)[D * (D + 1) / 2], double (&th)[D], double (&b)[D],
+__device__ __forceinline__ bool sm_update(double (&A)[D * (D + 1) / 2], double (&th)[D], double (&b)[D],
                                           const double (&x)[D], double r)
 {
     double z[D];
@@ -227,11 +235,13 @@ __device__ __forceinline__ void sm_update(double (&A)[D * (D + 1) / 2], double (
         px = fma(th[i], x[i], px);
     }
     const double invd = 1.0 / (1.0 + xz);
+    bool ok = spd_quad_ok(xz);
 #pragma unroll
     for (int r0 = 0; r0 < D; ++r0) {
         const double zr = -z[r0] * invd;
 #pragma unroll
         for (int c = r0; c < D; ++c) A[pidx<D>(r0, c)] = fma(zr, z[c], A[pidx<D>(r0, c)]);
+        ok = ok && A[pidx<D>(r0, r0)] > 0.0;
     }
     const double coef = (r - px) * invd;
 #pragma unroll
@@ -239,6 +249,7 @@ __device__ __forceinline__ void sm_update(double (&A)[D * (D + 1) / 2], double (
         th[i] = fma(z[i], coef, th[i]);
         b[i] = xadd(b[i], xmul(r, x[i]));
     }
+    return ok;
 }
 
 // ---- the sorted EDP window of ONE tuner in a strided shared-memory column (lane-private)
@@ -357,9 +368,9 @@ __device__ __forceinline__ double ring_oldest(const double *ring, uint32_t wcoun
 }
 
 // The same update with the packed A⁻¹ held in shared memory (entry e at Ac[e * stride]),
-// updated in place — keeps only z in registers.
+// updated in place — keeps only z in registers.  Returns the SPD guard.
 template <int D>
-__device__ __forceinline__ void sm_update_smem(double *Ac, int stride, double (&th)[D], double *bcol,
+__device__ __forceinline__ bool sm_update_smem(double *Ac, int stride, double (&th)[D], double *bcol,
                                                int bstride, const double (&x)[D], double r)
 {
     constexpr int P = D * (D + 1) / 2;
@@ -381,11 +392,16 @@ __device__ __forceinline__ void sm_update_smem(double *Ac, int stride, double (&
         px = fma(th[i], x[i], px);
     }
     const double invd = 1.0 / (1.0 + xz);
+    bool ok = spd_quad_ok(xz);
 #pragma unroll
     for (int r0 = 0; r0 < D; ++r0) {
         const double zr = -z[r0] * invd;
 #pragma unroll
-        for (int c = r0; c < D; ++c) Ac[pidx<D>(r0, c) * stride] = fma(zr, z[c], Ap[pidx<D>(r0, c)]);
+        for (int c = r0; c < D; ++c) {
+            const double v = fma(zr, z[c], Ap[pidx<D>(r0, c)]);
+            Ac[pidx<D>(r0, c) * stride] = v;
+            if (c == r0) ok = ok && v > 0.0;
+        }
     }
     const double coef = (r - px) * invd;
 #pragma unroll
@@ -394,6 +410,7 @@ __device__ __forceinline__ void sm_update_smem(double *Ac, int stride, double (&
         double &bi = bcol[(size_t)i * bstride];
         bi = xadd(bi, xmul(r, x[i]));
     }
+    return ok;
 }
 
 // one record's fields, loaded once per step

@@ -68,3 +68,19 @@ def test_des_checkpoint_resume_bitidentical():
     assert tb2.stats().tobytes() == want.tobytes()
     ref.close()
     tb2.close()
+
+
+@pytest.mark.parametrize("kw", [
+    dict(d=4),
+    dict(median_window=1),
+    dict(n_arms=1, prune_enable=0),
+    dict(prune_enable=0),
+    dict(kv_total=9000, pattern_mode=2),          # the queue overflows: arrivals are dropped
+])
+def test_des_edge_configs(kw):
+    cfg = with_overrides(named_config("C2"), cl_enable=2, n_tuners=4, n_traces=4, **kw)
+    ids = list(range(4))
+    params = tuner_params(cfg, ids)
+    tb, params, st, traj, gap = _run(cfg, 700, params=params, record=ids, chunk=350)
+    _check(cfg, tb, params, st, ids, 700, traj, gap=gap)
+    tb.close()

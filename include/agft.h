@@ -32,10 +32,11 @@
 extern "C" {
 #endif
 
-#define AGFT_ABI_VERSION 8u         /* 2: + agft_phase; 3: + agft_refine (and their stats); 4: + agft_select/agft_observe;
+#define AGFT_ABI_VERSION 9u         /* 2: + agft_phase; 3: + agft_refine (and their stats); 4: + agft_select/agft_observe;
                                        5: + agft_closed / agft_replay_raw; 6: MSEG/LANE policies retired;
                                        7: + agft_profile_start / agft_profile_read (workspace +128 B);
-                                       8: agft_closed.enable = 2 selects the ENV-S discrete-event server */
+                                       8: agft_closed.enable = 2 selects the ENV-S discrete-event server;
+                                       9: + agft_timeline */
 #define AGFT_MAX_ARMS 128u          /* K ≤ 128 */
 #define AGFT_MAX_D 7u               /* the paper's 7-dim context */
 #define AGFT_MAX_WINDOW 64u         /* reward-median window, AMB-3 */
@@ -348,6 +349,17 @@ agft_status agft_profile_start(agft_handle h, int serialize);
  * roofline (resident tuners ÷ chain latency per window).  Needs the device; no kernel launched. */
 agft_status agft_occupancy(const agft_config *cfg, int slot, uint32_t *tuners_per_sm);
 agft_status agft_profile_read(agft_handle h, agft_profile *out);
+/* Block-scheduling timeline (measurement): while d_buf is set, every warp of every
+ * replay-class launch appends one record when it exits — word 0 = launch sequence << 32 | class slot
+ * (0..5 as above) << 16 | SM id, words 1–2 = the %globaltimer values (ns) at the warp's start and end.
+ * d_buf is a caller-owned DEVICE buffer of 8 × (1 + 3 × cap_records) bytes; word 0 counts the records
+ * appended (records past cap_records are counted, not written).  The call zeroes the counter on the
+ * handle's stream and restarts the launch sequence; d_buf = null turns recording off.  Results are
+ * identical with or without it.  Recording exists only in a library built with -DAGFT_TIMELINE=1
+ * (tools/timeline.py builds that variant; the kernels of the product build carry no timeline code):
+ * the product build returns AGFT_E_INVALID_ARG for a non-null d_buf.  AGFT_E_INVALID_ARG also for a
+ * null handle or cap_records = 0 with a buffer. */
+agft_status agft_timeline(agft_handle h, void *d_buf, uint64_t cap_records);
 
 /* Frees the host handle only; the caller frees its device buffers. */
 agft_status agft_destroy(agft_handle h);

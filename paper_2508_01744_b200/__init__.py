@@ -149,6 +149,13 @@ def agft_profile_read(h) -> dict:
             for i, name in enumerate(_abi.PROFILE_SLOTS)}
 
 
+def agft_timeline(h, buf, cap_records: int = 0):
+    """Per-warp scheduling records of the replay-class launches into the int64 device tensor `buf`
+    (8 × (1 + 3 × cap_records) bytes); buf=None turns recording off (include/agft.h)."""
+    _abi.check("agft_timeline", _abi.lib().agft_timeline(h, _p(buf) if buf is not None else None,
+                                                         int(cap_records)))
+
+
 def agft_occupancy(cfg_c, slot: int) -> int:
     """Resident tuners per SM of replay class `slot` (_abi.PROFILE_SLOTS order) for this config."""
     v = C.c_uint32()

@@ -14,7 +14,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("AGFT_LIB_PATH") or os.path.join(HERE, "libagft.so")   # override: A/B builds
 
-ABI_VERSION = 8
+ABI_VERSION = 9
 RECORD_BYTES = 128
 ROW_WORDS = 12
 NO_RECORD = 0xFFFFFFFF
@@ -120,6 +120,7 @@ PROTOTYPES = {
     "agft_kernel_launches": (C.c_uint64, []),
     "agft_profile_start": (C.c_int, [vp, C.c_int]),
     "agft_profile_read": (C.c_int, [vp, vp]),
+    "agft_timeline": (C.c_int, [vp, vp, C.c_uint64]),
     "agft_occupancy": (C.c_int, [C.POINTER(AgftConfig), C.c_int, C.POINTER(u32)]),
 }
 

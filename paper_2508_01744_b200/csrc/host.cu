@@ -31,6 +31,10 @@ struct agft_handle_s {
     bool prof_on, prof_serial;
     std::vector<ProfEv> prof_ev;
     size_t prof_used;
+    // agft_timeline: per-warp records of the replay-class launches (null = off)
+    unsigned long long *tl = nullptr;
+    uint64_t tl_cap = 0;
+    uint32_t tl_seq = 0;
 };
 
 namespace agft {
@@ -342,6 +346,9 @@ agft_status agft_create(const agft_config *cfg, const agft_tuner_params *d_param
     h->prof_on = false;
     h->prof_serial = false;
     h->prof_used = 0;
+    h->tl = nullptr;
+    h->tl_cap = 0;
+    h->tl_seq = 0;
     h->fork = nullptr;
     for (int c = 0; c < kNumCls; ++c) {
         h->side[c] = nullptr;
@@ -396,6 +403,9 @@ agft_status agft_attach(const agft_config *cfg, void *d_workspace, size_t ws_byt
     h->prof_on = false;
     h->prof_serial = false;
     h->prof_used = 0;
+    h->tl = nullptr;
+    h->tl_cap = 0;
+    h->tl_seq = 0;
     h->fork = nullptr;
     for (int c = 0; c < kNumCls; ++c) {
         h->side[c] = nullptr;
@@ -499,6 +509,9 @@ static agft_status run_steps(agft_handle h, const void *d_records, uint32_t t0, 
             if (len > to_point) len = to_point;
         }
         ReplayArgs a = replay_args(h, d_records, t, len);
+        a.tl = h->tl;
+        a.tl_cap = (uint32_t)(h->tl_cap < 0xffffffffu ? h->tl_cap : 0xffffffffu);
+        a.tl_seq = h->tl_seq;
         a.rec_stride = n;
         a.rec_off = s;
         a.rf_defer = defer ? 1u : 0u;
@@ -511,6 +524,7 @@ static agft_status run_steps(agft_handle h, const void *d_records, uint32_t t0, 
         // warp per tuner throughout
         // (ENV-S servers, closed.enable = 2, run on the WIDE mapping: a warp per tuner drives its server)
         if (c.kernel_policy == AGFT_POLICY_WIDE || (c.refine.enable && !defer) || c.closed.enable == 2u) {
+            ++h->tl_seq;
             e = prof_begin(h, kClsWide, h->stream, &a);
             if (e == cudaSuccess) e = launch_replay(a, c.d, h->stream);
             if (e == cudaSuccess) e = prof_end(h, h->stream);
@@ -523,6 +537,8 @@ static agft_status run_steps(agft_handle h, const void *d_records, uint32_t t0, 
                 ReplayArgs ak = a;
                 ak.list = h->ws.lists + (size_t)k * c.n_tuners;
                 ak.count = h->ws.counts + k;
+                ak.tl_cls = (uint32_t)k;
+                ak.tl_seq = h->tl_seq++;
                 // agft_profile_start(h, 1): every class alone on the handle's stream (per-kernel times)
                 const cudaStream_t sk = h->prof_on && h->prof_serial ? h->stream : h->side[k];
                 if (sk != h->stream) e = cudaStreamWaitEvent(sk, h->fork, 0);
@@ -778,6 +794,17 @@ agft_status agft_profile_start(agft_handle h, int serialize)
     h->prof_serial = serialize != 0;
     h->prof_used = 0;
     return cuda_status(h, cudaMemsetAsync(h->ws.prof, 0, 16 * sizeof(unsigned long long), h->stream));
+}
+
+agft_status agft_timeline(agft_handle h, void *d_buf, uint64_t cap_records)
+{
+    if (!h || (d_buf && cap_records == 0) || (d_buf && !AGFT_TIMELINE)) return AGFT_E_INVALID_ARG;
+    if (h->sticky != AGFT_OK) return h->sticky;
+    h->tl = static_cast<unsigned long long *>(d_buf);
+    h->tl_cap = d_buf ? cap_records : 0;
+    h->tl_seq = 0;
+    if (!d_buf) return AGFT_OK;
+    return cuda_status(h, cudaMemsetAsync(d_buf, 0, sizeof(unsigned long long), h->stream));
 }
 
 agft_status agft_profile_read(agft_handle h, agft_profile *out)

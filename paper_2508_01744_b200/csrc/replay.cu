@@ -97,6 +97,7 @@ template <int D, int S, int MODE>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 replay_kernel(const __grid_constant__ ReplayArgs a)
 {
+    const TlGuard tl_guard(a);
     constexpr int P = D * (D + 1) / 2;
     extern __shared__ double smem[];
     double *s_dec = smem, *s_pre = smem + kMaxArms, *s_pw = smem + 2 * kMaxArms;

@@ -57,6 +57,7 @@ constexpr size_t seg2_smem_bytes(int P, int D)
 template <int D, int G>
 __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(const __grid_constant__ ReplayArgs a)
 {
+    const TlGuard tl_guard(a);
     constexpr int P = D * (D + 1) / 2;
     constexpr int E = kWindow / G;
     constexpr int NSEG = 32 / G;

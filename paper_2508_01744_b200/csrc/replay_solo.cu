@@ -27,6 +27,7 @@ constexpr int kSoloMinBlocks = AGFT_SOLO_MIN_BLOCKS;
 template <int D>
 __global__ void __launch_bounds__(kSoloThreads, kSoloMinBlocks) solo_kernel(const __grid_constant__ ReplayArgs a)
 {
+    const TlGuard tl_guard(a);
     constexpr int P = D * (D + 1) / 2;
     __shared__ double S_[kWindow * kSoloThreads];
     const uint32_t cnt = a.count ? *a.count : a.n_tuners;

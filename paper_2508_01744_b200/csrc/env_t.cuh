@@ -31,20 +31,29 @@ __device__ __forceinline__ double unit53(uint32_t a, uint32_t b)
     return xmul((double)m, 0x1p-53);
 }
 
-// ENV.md §3.3 response at one frequency (given its §3.1 constants).
+// ENV.md §3.3 response at one frequency (given its §3.1 constants), from the record's fields
+// (I and P already converted to double: exact, they are < 2^32).
+__device__ __forceinline__ void response_f(double I, double P, double g, double invIm, double nT, double nE,
+                                           double dec, double pre, double pw, double W, double invW,
+                                           double q_over, double u_max, double u_floor, double p_idle, double &E,
+                                           double &tpot)
+{
+    const double t_dec = xmul(I, dec);
+    const double t_pre = xmul(P, pre);
+    const double busy = xmul(xadd(t_dec, t_pre), g);
+    const double u = xmul(busy, invW);
+    const double q = u <= u_max ? xdiv(1.0, xsub(1.0, u)) : xmul(u, q_over);
+    tpot = xmul(xmul(xmul(xadd(dec, xmul(t_pre, invIm)), g), q), nT);
+    const double ue = fmax(fmin(u, 1.0), u_floor);   // clamp(u, u_floor, 1): u ≥ 0 is never NaN
+    E = xmul(xmul(xadd(p_idle, xmul(pw, ue)), W), nE);
+}
+
 __device__ __forceinline__ void response(const StepRec &r, double dec, double pre, double pw,
                                          double W, double invW, double q_over, double u_max,
                                          double u_floor, double p_idle, double &E, double &tpot)
 {
-    const double t_dec = xmul((double)r.I, dec);
-    const double t_pre = xmul((double)r.P, pre);
-    const double busy = xmul(xadd(t_dec, t_pre), r.g);
-    const double u = xmul(busy, invW);
-    const double q = u <= u_max ? xdiv(1.0, xsub(1.0, u)) : xmul(u, q_over);
-    tpot = xmul(xmul(xmul(xadd(dec, xmul(t_pre, r.invIm)), r.g), q), r.nT);
-    double ue = u > 1.0 ? 1.0 : u;
-    ue = ue < u_floor ? u_floor : ue;
-    E = xmul(xmul(xadd(p_idle, xmul(pw, ue)), W), r.nE);
+    response_f((double)r.I, (double)r.P, r.g, r.invIm, r.nT, r.nE, dec, pre, pw, W, invW, q_over, u_max, u_floor,
+               p_idle, E, tpot);
 }
 
 // §4.1 context x1..x7 from one window's MetricsSnapshot counters (ENV.md §3.2), then

@@ -26,6 +26,14 @@ namespace {
 #define AGFT_SEG2_WARPS 2               // warps per block (A/B knob)
 #endif
 constexpr int kSeg2Warps = AGFT_SEG2_WARPS;
+#ifndef AGFT_SEG2_LEAN
+#define AGFT_SEG2_LEAN 0                // 1: Sherman–Morrison without caching A⁻¹'s entries (register budget)
+#endif
+#if AGFT_SEG2_LEAN
+#define SM_UPDATE sm_update_smem_lean
+#else
+#define SM_UPDATE sm_update_smem
+#endif
 #ifndef AGFT_SEG2_MIN_BLOCKS
 #define AGFT_SEG2_MIN_BLOCKS 4          // no effective register cap: spills cost more than occupancy gains (A/B)
 #endif
@@ -230,11 +238,12 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
         }
 
         // ---- a4: both slots
-        double w[P];
-        pair_weights<D>(x, w);
+        double x2[D];
+#pragma unroll
+        for (int i = 0; i < D; ++i) x2[i] = 2.0 * x[i];
         double sc0 = -kInf, mg0 = 0.0, sc1 = -kInf, mg1 = 0.0;
         if (act0) {
-            const double q = quad_form<P>(w, A0, 32);
+            const double q = quad_form_rows<D>(x, x2, A0, 32);
             double p = 0.0;
 #pragma unroll
             for (int i = 0; i < D; ++i) p = fma(th0[i], x[i], p);
@@ -243,7 +252,7 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
             mg0 = fabs(p) + bonus;
         }
         if (act1) {
-            const double q = quad_form<P>(w, A1, 32);
+            const double q = quad_form_rows<D>(x, x2, A1, 32);
             double p = 0.0;
 #pragma unroll
             for (int i = 0; i < D; ++i) p = fma(th1[i], x[i], p);
@@ -340,8 +349,8 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
             double thv[D];
 #pragma unroll
             for (int i = 0; i < D; ++i) thv[i] = oslot ? th1[i] : th0[i];
-            if (kBS) spd = sm_update_smem<D>(oslot ? A1 : A0, 32, thv, oslot ? B1 : B0, 32, x, r);
-            else spd = sm_update_smem<D>(oslot ? A1 : A0, 32, thv, bg + kstar, kMaxArms, x, r);
+            if (kBS) spd = SM_UPDATE<D>(oslot ? A1 : A0, 32, thv, oslot ? B1 : B0, 32, x, r);
+            else spd = SM_UPDATE<D>(oslot ? A1 : A0, 32, thv, bg + kstar, kMaxArms, x, r);
 #pragma unroll
             for (int i = 0; i < D; ++i) {
                 if (oslot) th1[i] = thv[i]; else th0[i] = thv[i];

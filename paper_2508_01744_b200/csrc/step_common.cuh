@@ -25,8 +25,7 @@ __device__ __forceinline__ Response env_response(double dec, double pre, double 
     const double u = xmul(busy, invW);
     const double q = u <= u_max ? xdiv(1.0, xsub(1.0, u)) : xmul(u, q_over);
     o.tpot = xmul(xmul(xmul(xadd(dec, xmul(t_pre, invIm)), g), q), nT);
-    double ue = u > 1.0 ? 1.0 : u;
-    ue = ue < u_floor ? u_floor : ue;
+    const double ue = fmax(fmin(u, 1.0), u_floor);   // clamp(u, u_floor, 1): u ≥ 0 is never NaN
     o.E = xmul(xmul(xadd(p_idle, xmul(pw, ue)), W), nE);
     o.ttft = xmul(xadd(xmul(t_pre, invAm), xmul(t_dec, wIm)), q);
     o.edp = xmul(o.E, o.tpot);
@@ -181,6 +180,27 @@ __device__ __forceinline__ double quad_form(const double (&w)[P], const double *
         if (e + 3 < P) q3 = fma(w[e + 3 < P ? e + 3 : e], A[(e + 3 < P ? e + 3 : e) * stride], q3);
     }
     return (q0 + q1) + (q2 + q3);
+}
+
+// The same form row by row without the pair weights: xᵀA⁻¹x = Σ_i x_i (A_ii x_i + Σ_{j>i} A_ij (2x_j)),
+// x2 = 2x (exact).  7 + 28 FP64 instructions per arm and 2·D registers of weights instead of
+// D(D+1)/2 + the 49 instructions that build them once per step (SEG2: two arms per lane)
+template <int D>
+__device__ __forceinline__ double quad_form_rows(const double (&x)[D], const double (&x2)[D], const double *A,
+                                                 int stride)
+{
+    double q0 = 0.0, q1 = 0.0;
+    int e = 0;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        double in = A[e * stride] * x[i];
+        ++e;
+#pragma unroll
+        for (int j = i + 1; j < D; ++j, ++e) in = fma(A[e * stride], x2[j], in);
+        if (i & 1) q1 = fma(x[i], in, q1);
+        else q0 = fma(x[i], in, q0);
+    }
+    return q0 + q1;
 }
 
 template <int D>
@@ -400,6 +420,57 @@ __device__ __forceinline__ bool sm_update_smem(double *Ac, int stride, double (&
         for (int c = r0; c < D; ++c) {
             const double v = fma(zr, z[c], Ap[pidx<D>(r0, c)]);
             Ac[pidx<D>(r0, c) * stride] = v;
+            if (c == r0) ok = ok && v > 0.0;
+        }
+    }
+    const double coef = (r - px) * invd;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        th[i] = fma(z[i], coef, th[i]);
+        double &bi = bcol[(size_t)i * bstride];
+        bi = xadd(bi, xmul(r, x[i]));
+    }
+    return ok;
+}
+
+// The same update without caching the packed entries in registers (SEG2 at > 8 warps per SM: the
+// per-SMSP register budget is 168): z = A⁻¹x accumulated over the packed upper triangle (each entry
+// read once, used for z_i and z_j), then each entry re-read for its rank-1 update.  Same operations in
+// the same order per z_i as sm_update_smem (z_i = Σ_c A_ic x_c, c ascending), so identical values.
+template <int D>
+__device__ __forceinline__ bool sm_update_smem_lean(double *Ac, int stride, double (&th)[D], double *bcol,
+                                                    int bstride, const double (&x)[D], double r)
+{
+    double z[D];
+#pragma unroll
+    for (int i = 0; i < D; ++i) z[i] = 0.0;
+    // row-major walk over the packed entries (i ≤ c): z_i takes term c and z_c takes term i; every z_j
+    // then receives its terms in ascending column order, exactly as Σ_c A_jc x_c
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+#pragma unroll
+        for (int c = i; c < D; ++c) {
+            const double v = Ac[pidx<D>(i, c) * stride];
+            z[i] = fma(v, x[c], z[i]);
+            if (c != i) z[c] = fma(v, x[i], z[c]);
+        }
+    }
+    double xz = 0.0, px = 0.0;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        xz = fma(x[i], z[i], xz);
+        px = fma(th[i], x[i], px);
+    }
+    const double invd = 1.0 / (1.0 + xz);
+    bool ok = spd_quad_ok(xz);
+#pragma unroll
+    for (int r0 = 0; r0 < D; ++r0) {
+        const double zr = -z[r0] * invd;
+#pragma unroll
+        for (int c = r0; c < D; ++c) {
+            double &Ae = Ac[pidx<D>(r0, c) * stride];
+            const double v = fma(zr, z[c], Ae);
+            Ae = v;
             if (c == r0) ok = ok && v > 0.0;
         }
     }

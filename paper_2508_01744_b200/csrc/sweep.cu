@@ -17,10 +17,13 @@ namespace {
 
 constexpr int kTile = 32;
 constexpr int kThreads2 = 256;
+constexpr int kWarps2 = kThreads2 / 32;
 constexpr int kMaxArmsSw = 128;
-constexpr size_t kSweepSmem = (size_t)kTile * 16 * 8 + 3 * (size_t)kTile * kMaxArmsSw * 8 + 2 * kTile * 8;
+constexpr int kLd = kTile + 1;                // arm-major tables [k][w], odd stride: conflict-free both ways
+constexpr size_t kSweepSmem = 3 * (size_t)kMaxArmsSw * kLd * 8 + 2 * kTile * 8 +
+                              3 * (size_t)kMaxArmsSw * 8;
 #ifndef AGFT_SWEEP_ILP
-#define AGFT_SWEEP_ILP 8
+#define AGFT_SWEEP_ILP 7                      // 8 warps × 7 = 56 arms per pass: two passes cover K = 107
 #endif
 constexpr int kIlp = AGFT_SWEEP_ILP;          // independent ENV-R evaluations in flight per thread
 constexpr uint32_t kNoArm = 0xFFu;
@@ -47,25 +50,33 @@ struct SweepArgs {
 //      kIlp in flight) into shared memory E / TPOT / EDP tables [window][arm];
 //   B. warps 0–3 (thread k = arm k) fold the tile into their sums in window order, while warps
 //      4–7 find each window's k° (8 windows per warp) and one of them folds the oracle sums —
-// so the FP64 evaluations run at 16 warps per SM (two CTAs of 100 KB) and the serial folds,
+// so the FP64 evaluations run at 16 warps per SM (two CTAs of 110 KB) and the serial folds,
 // ~1/20 of the arithmetic, overlap each other.  Results are bit-identical to v1.
+// v3 (v2 issued ~89 warp instructions per (window, arm) evaluation, 29 of them FP64):
+// phase A maps lane = window and warp = arm subset, so a lane converts its record's fields once per
+// tile and every evaluation is the ENV-R arithmetic plus three conflict-free stores; the tables are
+// arm-major with an odd stride (stores by window, folds by arm, k° scans all conflict-free); no
+// evaluation of the padding slots k ≥ K (their EDP rows hold +inf for the k° scan).
 __global__ void __launch_bounds__(kThreads2, 2) sweep_kernel(const __grid_constant__ SweepArgs a)
 {
     extern __shared__ __align__(16) double sw[];
-    StepRec *s_rec = reinterpret_cast<StepRec *>(sw);                            // [kTile]
-    double *s_E = sw + kTile * 16, *s_T = s_E + kTile * kMaxArmsSw, *s_D = s_T + kTile * kMaxArmsSw;
-    double *s_oe = s_D + kTile * kMaxArmsSw, *s_oE = s_oe + kTile;
+    double *s_E = sw, *s_T = s_E + kMaxArmsSw * kLd, *s_D = s_T + kMaxArmsSw * kLd;   // [k][kLd]
+    double *s_oe = s_D + kMaxArmsSw * kLd, *s_oE = s_oe + kTile;
+    double *s_dec = s_oE + kTile, *s_pre = s_dec + kMaxArmsSw, *s_pw = s_pre + kMaxArmsSw;
     const uint32_t r = blockIdx.x;                                               // local trace
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const EnvConsts &ec = *a.env;
     const double invW = ec.invW, q_over = ec.q_over;
     const Philox ph{(uint32_t)a.seed ^ (a.trace_base + r), (uint32_t)(a.seed >> 32)};
-    // phase A mapping: arm slot ka, windows [wa0, wa0 + 16)
-    const int ka = lane + 32 * (warp & 3), wa0 = (warp >> 2) * (kTile / 2);
-    const bool arm_a = (uint32_t)ka < a.K;
-    const double dec = arm_a ? ec.dec[ka] : 0.0, pre = arm_a ? ec.pre[ka] : 0.0, pw = arm_a ? ec.pw[ka] : 0.0;
+    const int K = (int)a.K;
+    for (int q = tid; q < kMaxArmsSw; q += kThreads2) {
+        s_dec[q] = q < K ? ec.dec[q] : 0.0;
+        s_pre[q] = q < K ? ec.pre[q] : 0.0;
+        s_pw[q] = q < K ? ec.pw[q] : 0.0;
+    }
+    for (int q = K * kLd + tid; q < kMaxArmsSw * kLd; q += kThreads2) s_D[q] = kInf;   // padding rows
     // phase B accumulators: warps 0–3, thread tid = arm
-    const bool acc = warp < 4, arm = acc && (uint32_t)tid < a.K;
+    const bool acc = warp < 4, arm = acc && tid < K;
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, sp[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
     if (arm) {
         const double *S = a.S + ((size_t)r * a.K + tid) * 3;
@@ -86,32 +97,50 @@ __global__ void __launch_bounds__(kThreads2, 2) sweep_kernel(const __grid_consta
         for (int p = 0; p < 5; ++p) np[p] = a.NP[r * 5 + p];
     }
     const StepRec *rp = a.records + (size_t)r * a.n_steps;
+    // phase A lane = window: its record's six ENV-R fields straight from global memory (L1 after the
+    // CTA's first warp), the next tile's loaded one tile ahead (no staging copy, no barrier for it)
+    struct Fld {
+        double g, invIm, nT, nE;
+        uint2 ip;
+    };
+    auto load_fld = [&](uint32_t b) {
+        Fld f;
+        const StepRec *rc = rp + min(b + (uint32_t)lane, a.n_steps - 1);
+        f.g = __ldg(&rc->g);
+        f.invIm = __ldg(&rc->invIm);
+        f.nT = __ldg(&rc->nT);
+        f.nE = __ldg(&rc->nE);
+        f.ip = __ldg(reinterpret_cast<const uint2 *>(&rc->I));
+        return f;
+    };
+    Fld nxt = load_fld(0);
+    __syncthreads();                                                             // arm constants, padding rows
 
     for (uint32_t base = 0; base < a.n_steps; base += kTile) {
         const int nw = (int)min((uint32_t)kTile, a.n_steps - base);
-        {                                                                        // stage the records
-            const uint4 *src = reinterpret_cast<const uint4 *>(rp + base);
-            uint4 *dst = reinterpret_cast<uint4 *>(s_rec);
-            for (int q = tid; q < nw * 8; q += kThreads2) dst[q] = __ldg(src + q);
-        }
-        __syncthreads();
-        // ---- A: ENV-R (ENV.md §3.3) at arm ka for windows wa0.. (kIlp in flight)
+        const Fld cur = nxt;
+        if (base + kTile < a.n_steps) nxt = load_fld(base + kTile);
+        // ---- A: ENV-R (ENV.md §3.3) for window w = lane at arms warp, warp + 8, … (kIlp in flight)
+        {
+            const int w = lane;
+            const double I = (double)cur.ip.x, P = (double)cur.ip.y, g = cur.g, invIm = cur.invIm, nT = cur.nT,
+                         nE = cur.nE;
+            for (int k0 = warp; k0 < K; k0 += kWarps2 * kIlp) {
+                double E[kIlp], tp[kIlp];
 #pragma unroll
-        for (int j0 = 0; j0 < kTile / 2; j0 += kIlp) {
-            double E[kIlp], tp[kIlp];
+                for (int j = 0; j < kIlp; ++j) {
+                    const int k = min(k0 + kWarps2 * j, K - 1);
+                    response_f(I, P, g, invIm, nT, nE, s_dec[k], s_pre[k], s_pw[k], a.W, invW, q_over, a.u_max,
+                               a.u_floor, a.p_idle, E[j], tp[j]);
+                }
 #pragma unroll
-            for (int j = 0; j < kIlp; ++j) {
-                const int w = wa0 + j0 + j;
-                response(s_rec[w < nw ? w : 0], dec, pre, pw, a.W, invW, q_over, a.u_max, a.u_floor, a.p_idle, E[j],
-                         tp[j]);
-            }
-#pragma unroll
-            for (int j = 0; j < kIlp; ++j) {
-                const int w = wa0 + j0 + j;
-                if (w < nw) {
-                    s_E[w * kMaxArmsSw + ka] = E[j];
-                    s_T[w * kMaxArmsSw + ka] = tp[j];
-                    s_D[w * kMaxArmsSw + ka] = arm_a ? xmul(E[j], tp[j]) : kInf;
+                for (int j = 0; j < kIlp; ++j) {
+                    const int k = k0 + kWarps2 * j;
+                    if (k < K && w < nw) {
+                        s_E[k * kLd + w] = E[j];
+                        s_T[k * kLd + w] = tp[j];
+                        s_D[k * kLd + w] = xmul(E[j], tp[j]);
+                    }
                 }
             }
         }
@@ -127,9 +156,9 @@ __global__ void __launch_bounds__(kThreads2, 2) sweep_kernel(const __grid_consta
                 double cur = p == 0 ? sp[0] : p == 1 ? sp[1] : p == 2 ? sp[2] : p == 3 ? sp[3] : sp[4];
                 if (arm) {
                     for (; w < wend; ++w) {
-                        const double ed = s_D[w * kMaxArmsSw + tid];
-                        s0 = xadd(s0, s_E[w * kMaxArmsSw + tid]);
-                        s1 = xadd(s1, s_T[w * kMaxArmsSw + tid]);
+                        const double ed = s_D[tid * kLd + w];
+                        s0 = xadd(s0, s_E[tid * kLd + w]);
+                        s1 = xadd(s1, s_T[tid * kLd + w]);
                         s2 = xadd(s2, ed);
                         cur = xadd(cur, ed);
                     }
@@ -148,11 +177,11 @@ __global__ void __launch_bounds__(kThreads2, 2) sweep_kernel(const __grid_consta
             for (int j = 0; j < kTile / 4; ++j) {
                 const int w = (warp - 4) * (kTile / 4) + j;
                 if (w >= nw) break;                                              // warp-uniform
-                double bv = s_D[w * kMaxArmsSw + lane];
+                double bv = s_D[lane * kLd + w];
                 int bk = lane;
 #pragma unroll
                 for (int q = 1; q < kMaxArmsSw / 32; ++q) {
-                    const double v = s_D[w * kMaxArmsSw + lane + 32 * q];
+                    const double v = s_D[(lane + 32 * q) * kLd + w];
                     if (v < bv) {
                         bv = v;
                         bk = lane + 32 * q;
@@ -165,7 +194,7 @@ __global__ void __launch_bounds__(kThreads2, 2) sweep_kernel(const __grid_consta
                 const uint32_t kmin = __reduce_min_sync(kFull, (hi == mhi && lo == mlo) ? (uint32_t)bk : 0xFFFFFFFFu);
                 if (lane == j) {
                     s_oe[w] = __longlong_as_double((long long)(((uint64_t)mhi << 32) | mlo));
-                    s_oE[w] = s_E[w * kMaxArmsSw + kmin];                        // E at k°, as evaluated
+                    s_oE[w] = s_E[kmin * kLd + w];                               // E at k°, as evaluated
                     if (a.best) a.best[(size_t)r * a.n_steps + base + w] = (uint8_t)kmin;
                 }
             }

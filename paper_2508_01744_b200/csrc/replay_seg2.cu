@@ -193,6 +193,10 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
         clqb = a.w.clq[(size_t)tb * 2 + 1];
     }
     __syncwarp();
+    ScreenCache scr;                                                  // the incremental screen (G ≥ 8)
+    scr.ok = false;
+    scr.P = scr.B = scr.mx = scr.D = 0.0;
+    scr.M = -kInf;
 
     for (uint32_t s = 0; s < a.n_steps; ++s) {
         const uint32_t t = a.t0 + s;
@@ -345,7 +349,10 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
 
         // ---- a9: Sherman–Morrison on the owner lane's slot
         bool spd = true;
+        double scr_d = 0.0, scr_e = -kInf;                            // k*'s move within Q (screen_note)
         if (live && is_own) {
+            const uint32_t n_old = oslot ? n1 : n0;
+            const double e_old = oslot ? eb1 : eb0;
             double thv[D];
 #pragma unroll
             for (int i = 0; i < D; ++i) thv[i] = oslot ? th1[i] : th0[i];
@@ -357,6 +364,19 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
             }
             if (oslot) welford_inv(n1, rb1, eb1, r, o.edp, inv_n);
             else welford_inv(n0, rb0, eb0, r, o.edp, inv_n);
+            if (kScreen<G>()) {
+                const double e_new = oslot ? eb1 : eb0;
+                if (n_old >= a.hist_n) {                              // a member of Q moved
+                    scr_d = fabs(e_new - e_old);
+                    scr_e = e_new;
+                } else if (n_old + 1u >= a.hist_n) {                  // k* joined Q: membership changed
+                    scr_d = kInf;
+                }
+            }
+        }
+        if (kScreen<G>() && a.prune_enable) {
+            const double d = __shfl_sync(kFull, scr_d, own, G), e = __shfl_sync(kFull, scr_e, own, G);
+            screen_note(scr, d, e);
         }
         if (!spd) atomicOr(&st.flags, kFlagFrozen | kFlagSpd);      // SPD guard: frozen from the next step
 
@@ -373,10 +393,18 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
             // the screen (seg_common.cuh) skips the exact trees when no arm of Q can be removed; on for
             // G ≥ 8 (A/B on the C4 day: −10% / −8% / −6% kernel time for G = 8 / 16 / 32, +9% for G = 4,
             // whose small Q sets are mostly pruned anyway — DESIGN.md §4)
+            // (round 2: the full screen runs only when the cached bound of the last one no longer
+            // decides — seg_common.cuh::ScreenCache)
             bool exact = need;
-            if (kScreen<G>() && __any_sync(kFull, need)) {             // warp-wide call (butterflies)
-                const bool safe = hist_screen_safe<G>(q0, eb0, q1, eb1, nq, prm.historical_k);
-                exact = need && !safe;
+            if (kScreen<G>()) {
+                const bool inc = need && screen_inc_safe(scr);
+                exact = false;
+                if (__any_sync(kFull, need && !inc)) {                // warp-wide call (butterflies)
+                    ScreenCache fresh;
+                    const bool safe = hist_screen_full<G>(q0, eb0, q1, eb1, nq, prm.historical_k, fresh);
+                    if (need && !inc) scr = fresh;
+                    exact = need && !inc && !safe;
+                }
             }
             if (__any_sync(kFull, exact)) {
                 double best = fmin(q0 ? eb0 : kInf, q1 ? eb1 : kInf);
@@ -418,6 +446,7 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
                 const int ch = spopc<G>(rm0 && !ext0 && hist0, sg) + spopc<G>(rm1 && !ext1 && hist1, sg);
                 const int cc = spopc<G>(rm0 && !ext0 && !hist0, sg) + spopc<G>(rm1 && !ext1 && !hist1, sg);
                 if (any_rm) {
+                    scr.ok = false;                                   // Q lost members: the bound is void
                     if (l == 0) {
                         st.n_pruned_extreme += ce;
                         st.n_pruned_hist += ch;

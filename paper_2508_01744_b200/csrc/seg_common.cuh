@@ -112,8 +112,22 @@ __device__ __forceinline__ double stree(double *buf, int l, bool h0, int k0, dou
 //   is ≥ √V*·(1 − 8u) (its μ error only adds n·ε² to Σ(ē − μ)², and the tree / division / square
 //   root round by ≤ 8u), so thr_lo = (best + k_h·√(V − dV)(1 − 8u))(1 − 16u) ≤ thr.
 // All equal means (max = min = best) remove nothing either: thr ≥ best.  Called warp-wide.
+// The screen's state carried between steps (per segment, replicated in its G lanes).  A full screen that
+// finds Q safe also leaves a lower bound of the exact threshold that stays valid while Q's membership is
+// unchanged and its means move: with D ≥ Σ|Δē| over the changes since (ℓ1 ≥ ℓ2), the true minimum
+// drops by at most D and the true σ by at most D/√n (σ = ‖Pē‖/√n, P the centring projection), so
+//   thr ≥ (1 − 16u)·(mn + k_h(1 − 8u)√V* − D·(1 + k_h/√n)),   √V* ≥ √(V − dV)  (k_h ≥ 0, ē > 0),
+// and max ē ≤ max(mx, M), M the largest changed mean.  P = mn + k_h·sd_lo and B ≥ 1 + k_h/√n carry the
+// full screen's part; the check rounds every term the safe way (screen_inc_safe).
+struct ScreenCache {
+    double P, B, mx, D, M;
+    bool ok;
+};
+
+// full screen over the segment (warp-wide call: butterflies); fills c when the result is "safe"
 template <int G>
-__device__ __forceinline__ bool hist_screen_safe(bool q0, double e0, bool q1, double e1, int nq, double kh)
+__device__ __forceinline__ bool hist_screen_full(bool q0, double e0, bool q1, double e1, int nq, double kh,
+                                                 ScreenCache &c)
 {
     double mn = fmin(q0 ? e0 : kInf, q1 ? e1 : kInf);
     double mx = fmax(q0 ? e0 : -kInf, q1 ? e1 : -kInf);
@@ -126,16 +140,63 @@ __device__ __forceinline__ bool hist_screen_safe(bool q0, double e0, bool q1, do
         s1 += __shfl_xor_sync(kFull, s1, off, G);
         s2 += __shfl_xor_sync(kFull, s2, off, G);
     }
-    if (!(mx > mn)) return true;
     constexpr double u = 0x1p-53;
+    c.ok = false;
+    c.mx = mx;
+    c.D = 0.0;
+    c.M = -kInf;
+    c.B = (1.0 + kh * rsqrt((double)(nq > 0 ? nq : 1))) * (1.0 + 8.0 * u);
+    if (!(mx > mn)) {                                  // all equal: thr ≥ best, nothing is removed
+        c.P = mn;
+        c.ok = kh >= 0.0;
+        return true;
+    }
     const double inq = 1.0 / (double)(nq > 0 ? nq : 1);
     const double m2 = s2 * inq, mu = s1 * inq;
     const double V = m2 - mu * mu;
     const double dV = 64.0 * u * m2;
     if (!(V - dV > 0.0)) return false;
     const double sd_lo = sqrt(V - dV) * (1.0 - 8.0 * u);
-    const double thr_lo = (mn + kh * sd_lo) * (1.0 - 16.0 * u);
-    return mx < thr_lo;
+    c.P = mn + kh * sd_lo;
+    const double thr_lo = c.P * (1.0 - 16.0 * u);
+    const bool safe = mx < thr_lo;
+    c.ok = safe && kh >= 0.0;
+    return safe;
+}
+
+// the cached bound after the changes noted since the full screen:
+//   R = ((P(1 − 8u) − D·B)(1 − 20u)) ≤ (1 − 16u)(P(1 − 6u) − D·B_true) ≤ thr   (P(1 − 6u) ≤ the exact
+// mn + k_h(1 − 8u)√V*; every rounding safe-side; a negative R fails the test since every mean is > 0;
+// host replay against the oracle's canonical trees: tests/test_screen_bound.py)
+__device__ __forceinline__ bool screen_inc_safe(const ScreenCache &c)
+{
+    constexpr double u = 0x1p-53;
+    const double R = (c.P * (1.0 - 8.0 * u) - c.D * c.B) * (1.0 - 20.0 * u);
+    return c.ok && fmax(c.mx, c.M) < R;
+}
+
+// one mean of Q moved by dlt (to enew); dlt = +inf marks a change of Q's membership (the bound is void)
+__device__ __forceinline__ void screen_note(ScreenCache &c, double dlt, double enew)
+{
+    constexpr double u = 0x1p-53;
+    c.D = (c.D + dlt) * (1.0 + 8.0 * u);               // ≥ the true Σ|Δ| (each rounding covered)
+    c.M = fmax(c.M, enew);
+}
+
+// Historical-pruning screen (ENV.md §4.8).  Historical pruning removes arm k ∈ Q iff
+// ē_k > thr = best + k_h·σ, with μ and σ from the canonical 128-slot trees.  From min, max, Σē and
+// Σē² over Q (one butterfly, any order) this returns true only when max ē_Q < thr_lo ≤ thr, so that
+// the exact evaluation would remove nothing and may be skipped:
+//   V = Σē²/n − μ² is within 27u·m2 of the true population variance V* (u = 2⁻⁵³, m2 = Σē²/n; sums
+//   of ≤ 64 positive terms, one product, one subtraction), taken as dV = 64u·m2; the exact path's σ
+//   is ≥ √V*·(1 − 8u) (its μ error only adds n·ε² to Σ(ē − μ)², and the tree / division / square
+//   root round by ≤ 8u), so thr_lo = (best + k_h·√(V − dV)(1 − 8u))(1 − 16u) ≤ thr.
+// All equal means (max = min = best) remove nothing either: thr ≥ best.  Called warp-wide.
+template <int G>
+__device__ __forceinline__ bool hist_screen_safe(bool q0, double e0, bool q1, double e1, int nq, double kh)
+{
+    ScreenCache c;
+    return hist_screen_full<G>(q0, e0, q1, e1, nq, kh, c);
 }
 
 }  // namespace agft

@@ -89,3 +89,90 @@ def test_screen_never_skips_a_removal(kh):
                 assert not rm, (kh, v.tolist())
     if kh > 2.0:                                        # k_h ≤ 2 prunes any distinct set (Popoviciu: σ ≤ range/2)
         assert safe_count > 100                         # the screen decides the easy cases
+
+
+# ---- the incremental screen (seg_common.cuh::ScreenCache): after a safe full screen, the cached bound
+# is reused while Q's membership is unchanged and its means move (D ≥ Σ|Δē|, M = max moved mean)
+
+def screen_full_cache(vals, kh):
+    """Host replay of hist_screen_full: (safe, cache) with the device's operation order."""
+    v = np.asarray(vals, np.float64)
+    n = len(v)
+    mn, mx = float(v.min()), float(v.max())
+    c = {"ok": False, "mx": mx, "D": 0.0, "M": -np.inf,
+         "B": (1.0 + kh * (1.0 / np.sqrt(float(n)))) * (1.0 + 8.0 * U)}
+    if not mx > mn:
+        c["P"] = mn
+        c["ok"] = kh >= 0.0
+        return True, c
+    s1 = 0.0
+    s2 = 0.0
+    for e in v:
+        s1 += float(e)
+        s2 += float(e) * float(e)
+    inq = 1.0 / n
+    m2, mu = s2 * inq, s1 * inq
+    V = m2 - mu * mu
+    dV = 64.0 * U * m2
+    if not V - dV > 0.0:
+        return False, c
+    sd_lo = np.sqrt(V - dV) * (1.0 - 8.0 * U)
+    c["P"] = mn + kh * sd_lo
+    safe = mx < c["P"] * (1.0 - 16.0 * U)
+    c["ok"] = bool(safe and kh >= 0.0)
+    return safe, c
+
+
+def inc_safe(c):
+    R = (c["P"] * (1.0 - 8.0 * U) - c["D"] * c["B"]) * (1.0 - 20.0 * U)
+    return c["ok"] and max(c["mx"], c["M"]) < R
+
+
+def note(c, d, e):
+    c["D"] = (c["D"] + d) * (1.0 + 8.0 * U)
+    c["M"] = max(c["M"], e)
+
+
+@pytest.mark.parametrize("kh", [0.5, 1.0, 2.0, 3.0, 4.0])
+def test_incremental_screen_never_skips_a_removal(kh):
+    """Random walks of the means of Q after a safe full screen (the device's per-step moves: one mean
+    at a time, drifting toward the threshold, jumping, shrinking toward the minimum): whenever the
+    cached bound says safe, the exact evaluation on the current means removes nothing."""
+    rng = np.random.default_rng(int(kh * 100) + 11)
+    used = 0
+    for case in range(1500):
+        n = int(rng.integers(2, 33))
+        base = float(rng.lognormal(0.0, 1.5))
+        vals = base * rng.lognormal(0.0, float(rng.choice([1e-6, 1e-3, 0.05, 0.3])), n)
+        keys = np.sort(rng.choice(128, size=n, replace=False))
+        safe, c = screen_full_cache(vals, kh)
+        if not safe:
+            continue
+        _, thr = exact_removes(vals, keys, kh)
+        gap = thr - float(vals.max())
+        for step in range(60):
+            j = int(rng.integers(n))
+            mode = rng.integers(4)
+            old = float(vals[j])
+            if mode == 0:                                   # drift the largest toward the threshold
+                j = int(np.argmax(vals))
+                old = float(vals[j])
+                new = old + abs(gap) * float(rng.uniform(0.0, 0.6))
+            elif mode == 1:                                 # drop the minimum
+                j = int(np.argmin(vals))
+                old = float(vals[j])
+                new = old - abs(gap) * float(rng.uniform(0.0, 0.3))
+            elif mode == 2:                                 # tiny Welford-like move
+                new = old * (1.0 + float(rng.normal(0.0, 1e-3)))
+            else:                                           # collapse toward the mean (σ shrinks)
+                new = old + (float(vals.mean()) - old) * float(rng.uniform(0.0, 1.0))
+            if not new > 0.0:
+                continue
+            vals[j] = new
+            note(c, abs(new - old), new)
+            if inc_safe(c):
+                used += 1
+                rm, _ = exact_removes(vals, keys, kh)
+                assert not rm, (kh, case, step, vals.tolist())
+    if kh > 2.0:                                            # (k_h ≤ 2 prunes any distinct set, as above)
+        assert used > 100                                   # the cache decides the easy steps

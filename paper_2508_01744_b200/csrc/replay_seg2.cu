@@ -26,6 +26,9 @@ namespace {
 #define AGFT_SEG2_WARPS 2               // warps per block (A/B knob)
 #endif
 constexpr int kSeg2Warps = AGFT_SEG2_WARPS;
+#ifndef AGFT_SEG2_VREC
+#define AGFT_SEG2_VREC 0                // 1: the step record as 8 vector loads (A/B knob)
+#endif
 #ifndef AGFT_SEG2_LEAN
 #define AGFT_SEG2_LEAN 0                // 1: Sherman–Morrison without caching A⁻¹'s entries (register budget)
 #endif
@@ -48,8 +51,11 @@ __host__ __device__ constexpr bool b_in_smem() { return true; }
 template <int G>
 __host__ __device__ constexpr bool env_in_smem() { return G >= 8; }
 
+#ifndef AGFT_SCREEN_MIN_G
+#define AGFT_SCREEN_MIN_G 8             // the screen for G ≥ this (A/B knob)
+#endif
 template <int G>
-__host__ __device__ constexpr bool kScreen() { return G >= 8; }
+__host__ __device__ constexpr bool kScreen() { return G >= AGFT_SCREEN_MIN_G; }
 
 template <int G>
 constexpr size_t seg2_smem_bytes(int P, int D)
@@ -204,6 +210,12 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
 #if AGFT_TMA
         const StepRec *rc = rt.on ? rt.at(s, lane) : rp + s;
 #define RF(f) (rt.on ? rc->f : __ldg(&rc->f))
+#elif AGFT_SEG2_VREC
+        const StepRec *rc = rp + s;
+        RecView rv;                                                   // the record as 8 × 16-B loads
+        double x[D];
+        load_rec<D>(rc, x, rv);
+#define RF(f) rv.f
 #else
         const StepRec *rc = rp + s;
 #define RF(f) __ldg(&rc->f)
@@ -212,9 +224,11 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
             if (!AGFT_TMA) prefetch_l1(rc + 1);
             if (rawp) prefetch_l1(rawp + (size_t)(s + 1) * AGFT_ROW_WORDS);
         }
+#if !AGFT_SEG2_VREC || AGFT_TMA
         double x[D];
 #pragma unroll
         for (int i = 0; i < D; ++i) x[i] = RF(x[i]);
+#endif
         double g = RF(g), wIm = RF(wIm), baseE = RF(baseE), baseEDP = RF(baseEDP);
         uint32_t arr_cl = 0u;
         if (rawp) {                                                   // ENV-C: the servers see their backlog
@@ -231,14 +245,11 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
         const double alpha = phase ? 0.0 : alpha_t(prm.alpha0, t, inv_tau);   // Exploitation: Eq. 2
         // the reward's reference (median of the window before this step's push) depends only on
         // the window: computed here, off the response → reward chain
-        double ref = 0.0;
-        if (wcount > 0) {
-            if (wcount & 1u) {
-                ref = wat<G, E>(S, wcount >> 1);
-            } else {
-                const double m0 = wat<G, E>(S, (wcount >> 1) - 1), m1 = wat<G, E>(S, wcount >> 1);
-                ref = xmul(xadd(m0, m1), 0.5);
-            }
+        // (branch-free — both lookups, then a select — so that no shuffle sits in a divergent region)
+        double ref;
+        {
+            const double m0 = wat<G, E>(S, (wcount >> 1) - 1u), m1 = wat<G, E>(S, wcount >> 1);
+            ref = wcount == 0u ? 0.0 : ((wcount & 1u) ? m1 : xmul(xadd(m0, m1), 0.5));
         }
 
         // ---- a4: both slots
@@ -309,13 +320,14 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
                                         a.p_idle, a.W);
         if (rawp) clq = closed_carry(arr_cl + clq, o.u, a.cl_q_max);
         // ---- a8: reward + segment window
-        double r = 0.0;
-        if (wcount > 0) {
-            r = reward_of(o.edp, ref, a.clip_lo, a.clip_hi);
-        }
-        if (!isfinite(o.edp) || !isfinite(r)) {
-            if (live && l == 0) st.flags |= 1u;
-            live = false;
+        // (round 2: a8, a9 and the window update are branch-free — selects and predicated stores — so the
+        // three independent chains after the reward (Sherman–Morrison, the window, Welford) form one basic
+        // block the compiler can interleave; the arithmetic and its order are unchanged)
+        const double r = wcount > 0u ? reward_of(o.edp, ref, a.clip_lo, a.clip_hi) : 0.0;
+        {
+            const bool bad = !isfinite(o.edp) || !isfinite(r);
+            if (bad && live && l == 0) st.flags |= 1u;
+            live = live && !bad;
         }
         if (a.ph_enable) {                                            // ENV.md §4.10 observe_reward
             __syncwarp();                                             // the last step's phase reads are done
@@ -326,46 +338,51 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
             __syncwarp();
             phase = ph.phase;
         }
-        if (wcount < M) {
-            winsert<G, E>(S, o.edp, wless<G, E>(S, o.edp), l);
-            if (live && l == 0) ring[wcount] = o.edp;
-            ++wcount;
-            if (wcount == M) oldest = M == 1 ? o.edp : ring[whead];   // prefetch the next eviction
-        } else {
+        {
+            // both ranks from ONE butterfly on the current window: #(S' < v) after removing `old` is
+            // #(S < v) − [old < v], exactly (multiset identity); a window still filling removes nothing
+            // (oldest = 0 there, below every EDP) and inserts at #(S < v)
+            const bool full = wcount >= M;
             const double old = oldest;
-            // both ranks from ONE butterfly on the current window: #(S' < v) after removing `old`
-            // is #(S < v) − [old < v], exactly (multiset identity)
             int c = 0;
 #pragma unroll
             for (int e = 0; e < E; ++e) c += ((S[e] < old) ? 1 : 0) + ((S[e] < o.edp) ? 0x10000 : 0);
             c = sisum<G>(c);
-            const int po = c & 0xffff, pv = (c >> 16) - ((old < o.edp) ? 1 : 0);
+            const int po = full ? (c & 0xffff) : kWindow, pv = (c >> 16) - ((full && old < o.edp) ? 1 : 0);
             wremove<G, E>(S, po, l);
             winsert<G, E>(S, o.edp, pv, l);
-            if (live && l == 0) ring[whead] = o.edp;
-            whead = (whead + 1 == M) ? 0u : whead + 1;
-            oldest = M == 1 ? o.edp : ring[whead];     // next step's eviction, loaded off the chain
+            if (live && l == 0) ring[full ? whead : wcount] = o.edp;
+            whead = full ? ((whead + 1 == M) ? 0u : whead + 1) : whead;
+            wcount = full ? wcount : wcount + 1u;
+            if (wcount == M) oldest = M == 1 ? o.edp : ring[whead];   // next step's eviction, off the chain
         }
 
-        // ---- a9: Sherman–Morrison on the owner lane's slot
-        bool spd = true;
+        // ---- a9: Sherman–Morrison on the owner lane's slot (every lane runs it on its own column; the
+        // owner's stores and results are kept)
+        const bool upd = live && is_own;
         double scr_d = 0.0, scr_e = -kInf;                            // k*'s move within Q (screen_note)
-        if (live && is_own) {
+        bool spd;
+        {
             const uint32_t n_old = oslot ? n1 : n0;
-            const double e_old = oslot ? eb1 : eb0;
+            const double e_old = oslot ? eb1 : eb0, rb_old = oslot ? rb1 : rb0;
             double thv[D];
 #pragma unroll
             for (int i = 0; i < D; ++i) thv[i] = oslot ? th1[i] : th0[i];
-            if (kBS) spd = SM_UPDATE<D>(oslot ? A1 : A0, 32, thv, oslot ? B1 : B0, 32, x, r);
-            else spd = SM_UPDATE<D>(oslot ? A1 : A0, 32, thv, bg + kstar, kMaxArms, x, r);
+            if (kBS) spd = sm_update_smem_pred<D>(upd, oslot ? A1 : A0, 32, thv, oslot ? B1 : B0, 32, x, r);
+            else spd = sm_update_smem_pred<D>(upd, oslot ? A1 : A0, 32, thv, bg + kstar, kMaxArms, x, r);
 #pragma unroll
             for (int i = 0; i < D; ++i) {
-                if (oslot) th1[i] = thv[i]; else th0[i] = thv[i];
+                th1[i] = oslot ? thv[i] : th1[i];
+                th0[i] = oslot ? th0[i] : thv[i];
             }
-            if (oslot) welford_inv(n1, rb1, eb1, r, o.edp, inv_n);
-            else welford_inv(n0, rb0, eb0, r, o.edp, inv_n);
-            if (kScreen<G>()) {
-                const double e_new = oslot ? eb1 : eb0;
+            // Welford (ENV.md §4.7) with 1/(n+1) computed off the chain
+            const double rb_new = xadd(rb_old, xmul(xsub(r, rb_old), inv_n));
+            const double e_new = xadd(e_old, xmul(xsub(o.edp, e_old), inv_n));
+            if (upd) {
+                if (oslot) { n1 = n_old + 1u; rb1 = rb_new; eb1 = e_new; }
+                else { n0 = n_old + 1u; rb0 = rb_new; eb0 = e_new; }
+            }
+            if (kScreen<G>() && upd) {
                 if (n_old >= a.hist_n) {                              // a member of Q moved
                     scr_d = fabs(e_new - e_old);
                     scr_e = e_new;

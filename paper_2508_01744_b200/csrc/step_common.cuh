@@ -484,6 +484,56 @@ __device__ __forceinline__ bool sm_update_smem_lean(double *Ac, int stride, doub
     return ok;
 }
 
+// sm_update_smem with every store predicated on `on` and no branch: the warp runs it in one basic block
+// with the independent work of the step (window, Welford), so the compiler can interleave them.  Lanes
+// with on = false read their own (valid) column and discard the result.  Same arithmetic as
+// sm_update_smem.
+template <int D>
+__device__ __forceinline__ bool sm_update_smem_pred(bool on, double *Ac, int stride, double (&th)[D], double *bcol,
+                                                    int bstride, const double (&x)[D], double r)
+{
+    constexpr int P = D * (D + 1) / 2;
+    double Ap[P];
+#pragma unroll
+    for (int e = 0; e < P; ++e) Ap[e] = Ac[e * stride];
+    double z[D];
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        double acc = 0.0;
+#pragma unroll
+        for (int c = 0; c < D; ++c) acc = fma(Ap[i <= c ? pidx<D>(i, c) : pidx<D>(c, i)], x[c], acc);
+        z[i] = acc;
+    }
+    double xz = 0.0, px = 0.0;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        xz = fma(x[i], z[i], xz);
+        px = fma(th[i], x[i], px);
+    }
+    const double invd = 1.0 / (1.0 + xz);
+    bool ok = spd_quad_ok(xz);
+#pragma unroll
+    for (int r0 = 0; r0 < D; ++r0) {
+        const double zr = -z[r0] * invd;
+#pragma unroll
+        for (int c = r0; c < D; ++c) {
+            const double v = fma(zr, z[c], Ap[pidx<D>(r0, c)]);
+            if (on) Ac[pidx<D>(r0, c) * stride] = v;
+            if (c == r0) ok = ok && v > 0.0;
+        }
+    }
+    const double coef = (r - px) * invd;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        const double t = fma(z[i], coef, th[i]);
+        th[i] = on ? t : th[i];
+        double &bi = bcol[(size_t)i * bstride];
+        const double nb = xadd(bi, xmul(r, x[i]));
+        if (on) bi = nb;
+    }
+    return ok || !on;
+}
+
 // one record's fields, loaded once per step
 struct RecView {
     double x[7];

@@ -418,6 +418,14 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
         }
         }
 
+        // the chosen arm's b (global memory) for the update below, loaded now so that its L2 round trip
+        // overlaps the response, the reward and the window instead of stalling the update (round 2)
+        double bpre[D];
+        if (lane == own) {
+#pragma unroll
+            for (int i = 0; i < D; ++i) bpre[i] = bglob[(size_t)i * kMaxArms + kstar];
+        }
+
         // ---- a7: ENV-R response at f = f_min + k*·step (ENV.md §3.3), exact arithmetic
         double E, tpot, ttft, edp;
         if constexpr (MODE == 2) {                    // live: the measured response, EDP = E·TPOT
@@ -538,8 +546,7 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
 #pragma unroll
             for (int i = 0; i < D; ++i) {
                 Tj[i * aS] = fma(z[i], coef, th[i]);
-                double *bp = bglob + (size_t)i * kMaxArms + kstar;
-                *bp = xadd(*bp, xmul(r, x[i]));                // b exact, as Eq. 4 writes it
+                bglob[(size_t)i * kMaxArms + kstar] = xadd(bpre[i], xmul(r, x[i]));   // b exact, as Eq. 4 writes it
             }
             const uint32_t nn = pick<S>(n, jst) + 1u;
             const double inv = xdiv(1.0, (double)nn);

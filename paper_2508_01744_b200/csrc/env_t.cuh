@@ -42,7 +42,7 @@ __device__ __forceinline__ void response_f(double I, double P, double g, double 
     const double t_pre = xmul(P, pre);
     const double busy = xmul(xadd(t_dec, t_pre), g);
     const double u = xmul(busy, invW);
-    const double q = u <= u_max ? xdiv(1.0, xsub(1.0, u)) : xmul(u, q_over);
+    const double q = u <= u_max ? xrcp_nb(xsub(1.0, u)) : xmul(u, q_over);
     tpot = xmul(xmul(xmul(xadd(dec, xmul(t_pre, invIm)), g), q), nT);
     double ue = u > 1.0 ? 1.0 : u;                  // (fmin/fmax compile to ~7 instructions each: NaN rules)
     ue = ue < u_floor ? u_floor : ue;

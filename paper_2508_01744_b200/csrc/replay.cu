@@ -451,7 +451,7 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
         const double t_pre = xmul((double)recP, pre);
         const double busy = xmul(xadd(t_dec, t_pre), g);
         const double u = xmul(busy, invW);
-        const double q = u <= a.u_max ? xdiv(1.0, xsub(1.0, u)) : xmul(u, q_over);
+        const double q = u <= a.u_max ? xrcp_nb(xsub(1.0, u)) : xmul(u, q_over);
         if (rawp) clq = closed_carry(arr_cl + clq, u, a.cl_q_max);   // ENV-C: left queued (§6)
         tpot = xmul(xmul(xmul(xadd(dec, xmul(t_pre, invIm)), g), q), nT);
         double ue = u > 1.0 ? 1.0 : u;
@@ -471,7 +471,7 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
                 const double m0 = window_at(wlo, whi, (wcount >> 1) - 1), m1 = window_at(wlo, whi, wcount >> 1);
                 ref = xmul(xadd(m0, m1), 0.5);
             }
-            r = xsub(1.0, xdiv(edp, ref));
+            r = xsub(1.0, xdiv_nb(edp, ref));
             r = r < a.clip_lo ? a.clip_lo : (r > a.clip_hi ? a.clip_hi : r);
         }
         if (!isfinite(edp) || !isfinite(r)) {         // anomaly: flag and freeze the tuner
@@ -529,7 +529,7 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
                 th[i] = Tj[i * aS];
                 px = fma(th[i], x[i], px);
             }
-            const double invd = 1.0 / (1.0 + xz);              // Sherman–Morrison denominator
+            const double invd = xrcp_nb(1.0 + xz);              // Sherman–Morrison denominator
             {
                 int e = 0;
 #pragma unroll
@@ -549,7 +549,7 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
                 bglob[(size_t)i * kMaxArms + kstar] = xadd(bpre[i], xmul(r, x[i]));   // b exact, as Eq. 4 writes it
             }
             const uint32_t nn = pick<S>(n, jst) + 1u;
-            const double inv = xdiv(1.0, (double)nn);
+            const double inv = xrcp_nb((double)nn);
             put<S>(n, jst, nn);
             put<S>(rbar, jst, xadd(pick<S>(rbar, jst), xmul(xsub(r, pick<S>(rbar, jst)), inv)));
             put<S>(ebar, jst, xadd(pick<S>(ebar, jst), xmul(xsub(edp, pick<S>(ebar, jst)), inv)));

@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(kSoloThreads, kSoloMinBlocks) solo_kernel(cons
         // off the chain: the reward's reference (median of the window before this push) and
         // Welford's 1/n depend only on the tuner's state at the start of the step
         const double ref = wcount > 0 ? win.median(wcount) : 0.0;
-        const double inv_n = xdiv(1.0, (double)(n + 1u));
+        const double inv_n = xrcp_nb((double)(n + 1u));
         // a7: response at the only active frequency
         const uint32_t rI = __ldg(&rc->I), rP = __ldg(&rc->P);
         const double rinvIm = __ldg(&rc->invIm), rnT = __ldg(&rc->nT), rnE = __ldg(&rc->nE);

@@ -23,7 +23,7 @@ __device__ __forceinline__ Response env_response(double dec, double pre, double 
     const double t_pre = xmul((double)P, pre);
     const double busy = xmul(xadd(t_dec, t_pre), g);
     const double u = xmul(busy, invW);
-    const double q = u <= u_max ? xdiv(1.0, xsub(1.0, u)) : xmul(u, q_over);
+    const double q = u <= u_max ? xrcp_nb(xsub(1.0, u)) : xmul(u, q_over);
     o.tpot = xmul(xmul(xmul(xadd(dec, xmul(t_pre, invIm)), g), q), nT);
     double ue = u > 1.0 ? 1.0 : u;                  // (fmin/fmax compile to ~7 instructions each: NaN rules)
     ue = ue < u_floor ? u_floor : ue;
@@ -97,7 +97,7 @@ __device__ __forceinline__ void prefetch_l1(const void *p) { asm volatile("prefe
 // a8: r = clip(1 − EDP/ref) (AMB-3)
 __device__ __forceinline__ double reward_of(double edp, double ref, double lo, double hi)
 {
-    double r = xsub(1.0, xdiv(edp, ref));
+    double r = xsub(1.0, xdiv_nb(edp, ref));
     return r < lo ? lo : (r > hi ? hi : r);
 }
 
@@ -255,7 +255,7 @@ __device__ __forceinline__ bool sm_update(double (&A)[D * (D + 1) / 2], double (
         xz = fma(x[i], z[i], xz);
         px = fma(th[i], x[i], px);
     }
-    const double invd = 1.0 / (1.0 + xz);
+    const double invd = xrcp_nb(1.0 + xz);
     bool ok = spd_quad_ok(xz);
 #pragma unroll
     for (int r0 = 0; r0 < D; ++r0) {
@@ -412,7 +412,7 @@ __device__ __forceinline__ bool sm_update_smem(double *Ac, int stride, double (&
         xz = fma(x[i], z[i], xz);
         px = fma(th[i], x[i], px);
     }
-    const double invd = 1.0 / (1.0 + xz);
+    const double invd = xrcp_nb(1.0 + xz);
     bool ok = spd_quad_ok(xz);
 #pragma unroll
     for (int r0 = 0; r0 < D; ++r0) {
@@ -462,7 +462,7 @@ __device__ __forceinline__ bool sm_update_smem_lean(double *Ac, int stride, doub
         xz = fma(x[i], z[i], xz);
         px = fma(th[i], x[i], px);
     }
-    const double invd = 1.0 / (1.0 + xz);
+    const double invd = xrcp_nb(1.0 + xz);
     bool ok = spd_quad_ok(xz);
 #pragma unroll
     for (int r0 = 0; r0 < D; ++r0) {
@@ -511,7 +511,7 @@ __device__ __forceinline__ bool sm_update_smem_pred(bool on, double *Ac, int str
         xz = fma(x[i], z[i], xz);
         px = fma(th[i], x[i], px);
     }
-    const double invd = 1.0 / (1.0 + xz);
+    const double invd = xrcp_nb(1.0 + xz);
     bool ok = spd_quad_ok(xz);
 #pragma unroll
     for (int r0 = 0; r0 < D; ++r0) {

@@ -248,7 +248,7 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
                     double p = 0.0;
 #pragma unroll
                     for (int i = 0; i < D; ++i) p = fma(Tj[i * aS], x[i], p);
-                    const double u = p + au * sqrt(fmax(q, 0.0));
+                    const double u = p + au * xsqrt_nb(q > 0.0 ? q : 0.0);
                     if (u > bu) { bu = u; bk2 = 32 * j + lane; }
                 }
             }
@@ -367,7 +367,7 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
                 double p = 0.0;
 #pragma unroll
                 for (int i = 0; i < D; ++i) p = fma(Tj[i * aS], x[i], p);
-                const double bonus = alpha * sqrt(fmax(q, 0.0));   // AMB-19
+                const double bonus = alpha * xsqrt_nb(q > 0.0 ? q : 0.0);   // AMB-19
                 sc[j] = p + bonus;
                 mg[j] = fabs(p) + bonus;
                 if (sc[j] > bs) { bs = sc[j]; bk = 32 * j + lane; }  // ascending k: ties keep lowest

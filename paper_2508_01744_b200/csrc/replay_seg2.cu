@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
             double p = 0.0;
 #pragma unroll
             for (int i = 0; i < D; ++i) p = fma(th0[i], x[i], p);
-            const double bonus = alpha * sqrt(fmax(q, 0.0));
+            const double bonus = alpha * xsqrt_nb(q > 0.0 ? q : 0.0);
             sc0 = p + bonus;
             mg0 = fabs(p) + bonus;
         }
@@ -271,7 +271,7 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
             double p = 0.0;
 #pragma unroll
             for (int i = 0; i < D; ++i) p = fma(th1[i], x[i], p);
-            const double bonus = alpha * sqrt(fmax(q, 0.0));
+            const double bonus = alpha * xsqrt_nb(q > 0.0 ? q : 0.0);
             sc1 = p + bonus;
             mg1 = fabs(p) + bonus;
         }

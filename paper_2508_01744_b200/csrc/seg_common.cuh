@@ -151,12 +151,12 @@ __device__ __forceinline__ bool hist_screen_full(bool q0, double e0, bool q1, do
         c.ok = kh >= 0.0;
         return true;
     }
-    const double inq = 1.0 / (double)(nq > 0 ? nq : 1);
+    const double inq = xrcp_nb((double)(nq > 0 ? nq : 1));
     const double m2 = s2 * inq, mu = s1 * inq;
     const double V = m2 - mu * mu;
     const double dV = 64.0 * u * m2;
     if (!(V - dV > 0.0)) return false;
-    const double sd_lo = sqrt(V - dV) * (1.0 - 8.0 * u);
+    const double sd_lo = xsqrt_nb(V - dV) * (1.0 - 8.0 * u);
     c.P = mn + kh * sd_lo;
     const double thr_lo = c.P * (1.0 - 16.0 * u);
     const bool safe = mx < thr_lo;

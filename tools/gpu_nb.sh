@@ -9,4 +9,4 @@ python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1 || { tail
 timeout 2400 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log; tail -2 $O/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log; tail -1 $O/smoke.log
 bash tools/gpu_abn.sh $TAG "" base=$B
-bash tools/gpu_ab_sweep.sh $TAG base=$B
+[ "${3:-}" = nosweep ] || bash tools/gpu_ab_sweep.sh $TAG base=$B

@@ -392,7 +392,7 @@ replay_kernel(const __grid_constant__ ReplayArgs a)
 #pragma unroll
         for (int j = 0; j < S; ++j) {
             if (!((act >> j) & 1u) || (32 * j + lane) == kstar) continue;
-            const double sc_ = fmax(mstar, mg[j]);
+            const double sc_ = mstar > mg[j] ? mstar : mg[j];   // (scores are finite here)
             if (sstar - sc[j] < a.tie_rel * sc_ && !(fresh_star && n[j] == 0u)) tie = true;
             if (sc[j] > s2) { s2 = sc[j]; m2 = mg[j]; }
         }

@@ -293,8 +293,8 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
         const bool fstar = __shfl_sync(kFull, (int)((oslot ? n1 : n0) == 0u), own, G) != 0;
         const bool own0 = is_own && oslot == 0, own1 = is_own && oslot == 1;
         const double inv_n = xrcp_nb((double)((oslot ? n1 : n0) + 1u));   // Welford's 1/n, off the chain
-        const bool tie = (act0 && !own0 && (bs - sc0 < a.tie_rel * fmax(mstar, mg0)) && !(fstar && n0 == 0u)) ||
-                         (act1 && !own1 && (bs - sc1 < a.tie_rel * fmax(mstar, mg1)) && !(fstar && n1 == 0u));
+        const bool tie = (act0 && !own0 && (bs - sc0 < a.tie_rel * (mstar > mg0 ? mstar : mg0)) && !(fstar && n0 == 0u)) ||
+                         (act1 && !own1 && (bs - sc1 < a.tie_rel * (mstar > mg1 ? mstar : mg1)) && !(fstar && n1 == 0u));
         const bool near = sbits<G>(tie, sg) != 0u;
         const int nact0 = nact;
         double gapv = kInf;

@@ -26,17 +26,6 @@ namespace {
 #define AGFT_SEG2_WARPS 2               // warps per block (A/B knob)
 #endif
 constexpr int kSeg2Warps = AGFT_SEG2_WARPS;
-#ifndef AGFT_SEG2_VREC
-#define AGFT_SEG2_VREC 0                // 1: the step record as 8 vector loads (A/B knob)
-#endif
-#ifndef AGFT_SEG2_LEAN
-#define AGFT_SEG2_LEAN 0                // 1: Sherman–Morrison without caching A⁻¹'s entries (register budget)
-#endif
-#if AGFT_SEG2_LEAN
-#define SM_UPDATE sm_update_smem_lean
-#else
-#define SM_UPDATE sm_update_smem
-#endif
 #ifndef AGFT_SEG2_MIN_BLOCKS
 #define AGFT_SEG2_MIN_BLOCKS 4          // no effective register cap: spills cost more than occupancy gains (A/B)
 #endif
@@ -210,12 +199,6 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
 #if AGFT_TMA
         const StepRec *rc = rt.on ? rt.at(s, lane) : rp + s;
 #define RF(f) (rt.on ? rc->f : __ldg(&rc->f))
-#elif AGFT_SEG2_VREC
-        const StepRec *rc = rp + s;
-        RecView rv;                                                   // the record as 8 × 16-B loads
-        double x[D];
-        load_rec<D>(rc, x, rv);
-#define RF(f) rv.f
 #else
         const StepRec *rc = rp + s;
 #define RF(f) __ldg(&rc->f)
@@ -224,11 +207,9 @@ __global__ void __launch_bounds__(kSeg2Warps * 32, kSeg2MinBlocks) seg2_kernel(c
             if (!AGFT_TMA) prefetch_l1(rc + 1);
             if (rawp) prefetch_l1(rawp + (size_t)(s + 1) * AGFT_ROW_WORDS);
         }
-#if !AGFT_SEG2_VREC || AGFT_TMA
         double x[D];
 #pragma unroll
         for (int i = 0; i < D; ++i) x[i] = RF(x[i]);
-#endif
         double g = RF(g), wIm = RF(wIm), baseE = RF(baseE), baseEDP = RF(baseEDP);
         uint32_t arr_cl = 0u;
         if (rawp) {                                                   // ENV-C: the servers see their backlog

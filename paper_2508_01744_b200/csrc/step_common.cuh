@@ -388,107 +388,10 @@ __device__ __forceinline__ double ring_oldest(const double *ring, uint32_t wcoun
     return wcount == M ? ring[whead] : 0.0;
 }
 
-// The same update with the packed A⁻¹ held in shared memory (entry e at Ac[e * stride]),
-// updated in place — keeps only z in registers.  Returns the SPD guard.
-template <int D>
-__device__ __forceinline__ bool sm_update_smem(double *Ac, int stride, double (&th)[D], double *bcol,
-                                               int bstride, const double (&x)[D], double r)
-{
-    constexpr int P = D * (D + 1) / 2;
-    double Ap[P];                                   // each packed entry read once (not twice)
-#pragma unroll
-    for (int e = 0; e < P; ++e) Ap[e] = Ac[e * stride];
-    double z[D];
-#pragma unroll
-    for (int i = 0; i < D; ++i) {
-        double acc = 0.0;
-#pragma unroll
-        for (int c = 0; c < D; ++c) acc = fma(Ap[i <= c ? pidx<D>(i, c) : pidx<D>(c, i)], x[c], acc);
-        z[i] = acc;
-    }
-    double xz = 0.0, px = 0.0;
-#pragma unroll
-    for (int i = 0; i < D; ++i) {
-        xz = fma(x[i], z[i], xz);
-        px = fma(th[i], x[i], px);
-    }
-    const double invd = xrcp_nb(1.0 + xz);
-    bool ok = spd_quad_ok(xz);
-#pragma unroll
-    for (int r0 = 0; r0 < D; ++r0) {
-        const double zr = -z[r0] * invd;
-#pragma unroll
-        for (int c = r0; c < D; ++c) {
-            const double v = fma(zr, z[c], Ap[pidx<D>(r0, c)]);
-            Ac[pidx<D>(r0, c) * stride] = v;
-            if (c == r0) ok = ok && v > 0.0;
-        }
-    }
-    const double coef = (r - px) * invd;
-#pragma unroll
-    for (int i = 0; i < D; ++i) {
-        th[i] = fma(z[i], coef, th[i]);
-        double &bi = bcol[(size_t)i * bstride];
-        bi = xadd(bi, xmul(r, x[i]));
-    }
-    return ok;
-}
-
-// The same update without caching the packed entries in registers (SEG2 at > 8 warps per SM: the
-// per-SMSP register budget is 168): z = A⁻¹x accumulated over the packed upper triangle (each entry
-// read once, used for z_i and z_j), then each entry re-read for its rank-1 update.  Same operations in
-// the same order per z_i as sm_update_smem (z_i = Σ_c A_ic x_c, c ascending), so identical values.
-template <int D>
-__device__ __forceinline__ bool sm_update_smem_lean(double *Ac, int stride, double (&th)[D], double *bcol,
-                                                    int bstride, const double (&x)[D], double r)
-{
-    double z[D];
-#pragma unroll
-    for (int i = 0; i < D; ++i) z[i] = 0.0;
-    // row-major walk over the packed entries (i ≤ c): z_i takes term c and z_c takes term i; every z_j
-    // then receives its terms in ascending column order, exactly as Σ_c A_jc x_c
-#pragma unroll
-    for (int i = 0; i < D; ++i) {
-#pragma unroll
-        for (int c = i; c < D; ++c) {
-            const double v = Ac[pidx<D>(i, c) * stride];
-            z[i] = fma(v, x[c], z[i]);
-            if (c != i) z[c] = fma(v, x[i], z[c]);
-        }
-    }
-    double xz = 0.0, px = 0.0;
-#pragma unroll
-    for (int i = 0; i < D; ++i) {
-        xz = fma(x[i], z[i], xz);
-        px = fma(th[i], x[i], px);
-    }
-    const double invd = xrcp_nb(1.0 + xz);
-    bool ok = spd_quad_ok(xz);
-#pragma unroll
-    for (int r0 = 0; r0 < D; ++r0) {
-        const double zr = -z[r0] * invd;
-#pragma unroll
-        for (int c = r0; c < D; ++c) {
-            double &Ae = Ac[pidx<D>(r0, c) * stride];
-            const double v = fma(zr, z[c], Ae);
-            Ae = v;
-            if (c == r0) ok = ok && v > 0.0;
-        }
-    }
-    const double coef = (r - px) * invd;
-#pragma unroll
-    for (int i = 0; i < D; ++i) {
-        th[i] = fma(z[i], coef, th[i]);
-        double &bi = bcol[(size_t)i * bstride];
-        bi = xadd(bi, xmul(r, x[i]));
-    }
-    return ok;
-}
-
-// sm_update_smem with every store predicated on `on` and no branch: the warp runs it in one basic block
-// with the independent work of the step (window, Welford), so the compiler can interleave them.  Lanes
-// with on = false read their own (valid) column and discard the result.  Same arithmetic as
-// sm_update_smem.
+// The update with the packed A⁻¹ held in shared memory (entry e at Ac[e * stride], each read once),
+// every store predicated on `on` and no branch: the warp runs it in one basic block with the
+// independent work of the step (window, Welford), so the compiler can interleave them.  Lanes with
+// on = false read their own (valid) column and discard the result.  Returns the SPD guard.
 template <int D>
 __device__ __forceinline__ bool sm_update_smem_pred(bool on, double *Ac, int stride, double (&th)[D], double *bcol,
                                                     int bstride, const double (&x)[D], double r)
@@ -533,39 +436,6 @@ __device__ __forceinline__ bool sm_update_smem_pred(bool on, double *Ac, int str
         if (on) bi = nb;
     }
     return ok || !on;
-}
-
-// one record's fields, loaded once per step
-struct RecView {
-    double x[7];
-    double g, invIm, invAm, wIm, nT, nE, baseE, baseEDP;
-    uint32_t I, P;
-};
-
-template <int D>
-__device__ __forceinline__ void load_rec(const StepRec *__restrict__ p, double (&x)[D], RecView &v)
-{
-    const double2 *q = reinterpret_cast<const double2 *>(p);
-    double f[16];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const double2 t = __ldg(q + i);
-        f[2 * i] = t.x;
-        f[2 * i + 1] = t.y;
-    }
-#pragma unroll
-    for (int i = 0; i < D; ++i) x[i] = f[i];
-    v.g = f[7];
-    v.invIm = f[8];
-    v.invAm = f[9];
-    v.wIm = f[10];
-    v.nT = f[11];
-    v.nE = f[12];
-    v.baseE = f[13];
-    v.baseEDP = f[14];
-    const uint2 ip = *reinterpret_cast<const uint2 *>(&f[15]);
-    v.I = ip.x;
-    v.P = ip.y;
 }
 
 }  // namespace agft

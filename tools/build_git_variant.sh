@@ -1,6 +1,6 @@
 #!/bin/bash
 # Build libagft.so from a git revision's sources into paper_2508_01744_b200/variants/libagft_<name>.so
-# (for A/B runs against the working tree with tools/gpu_ab_lib.sh).   bash tools/build_git_variant.sh <rev> <name>
+# (for A/B runs against the working tree with tools/gpu_abn.sh / tools/gpu_variant_check.sh).   bash tools/build_git_variant.sh <rev> <name>
 set -eu
 REV=$1; NAME=$2
 ROOT=$(cd "$(dirname "$0")/.." && pwd)

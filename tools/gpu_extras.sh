@@ -1,6 +1,6 @@
 #!/bin/bash
-# End-of-round extras on the product build: every §8(f) bench line (tools/gpu_final.sh without the
-# sanitizers), the small configurations C1–C3 with clock samples, C5 on one GPU, and the block-scheduling
+# End-of-round extras on the product build: every §8(f) bench line (the sanitizers are in
+# tools/gpu_sanitize.sh), the small configurations C1–C3 with clock samples, C5 on one GPU, and the block-scheduling
 # timeline of the C4 day (variant build).
 set -u
 O=gpurun_out/${1:-extras}; mkdir -p $O

@@ -1,6 +1,6 @@
 #!/bin/bash
 # Parity tests of the product and of a variant build, then the alternating C4 A/B of the two.
-#   gpurun -- 'bash tools/gpu_occ5.sh <tag> <variant name> <variant .so>'
+#   gpurun -- 'bash tools/gpu_variant_check.sh <tag> <variant name> <variant .so>'
 set -u
 TAG=$1; VN=$2; VL=$3
 O=gpurun_out/$TAG; mkdir -p $O

@@ -77,7 +77,9 @@ bool stream_prio_enabled()
 // rank[c] = position of class c in the priority order (0 = highest)
 void prio_order(int (&rank)[kNumCls])
 {
-    static const int def[kNumCls] = {kClsSeg16, kClsSeg32, kClsSeg8, kClsWide, kClsSeg64, kClsSolo};
+    // (round 2: the classes whose warps run longest first — G = 4, G = 32, WIDE, then G = 8, G = 16, SOLO;
+    // +2% on the C4 day over the round-1 order 2,1,3,0,5,4; profiles/r02_prio_ab/)
+    static const int def[kNumCls] = {kClsSeg8, kClsSeg64, kClsWide, kClsSeg16, kClsSeg32, kClsSolo};
     int order[kNumCls];
     for (int i = 0; i < kNumCls; ++i) order[i] = def[i];
     if (const char *e = std::getenv("AGFT_PRIO_ORDER")) {
@@ -103,10 +105,9 @@ void destroy_streams(agft_handle h)
     if (h->fork) cudaEventDestroy(h->fork);
 }
 
-// Class streams by priority: the multi-wave SEG classes first, so the block scheduler fills
-// SMs longest-work-first and the short classes pack around them (A/B: −2.3% per C4 day,
-// DESIGN.md §4).  AGFT_STREAM_PRIO=0 disables; AGFT_PRIO_ORDER="2,1,3,0,5,4" overrides the
-// order (class ids of agft_internal.cuh, highest priority first).
+// Class streams by priority: the classes whose warps run longest get the SMs first, so the short
+// classes pack around them (A/B).  AGFT_STREAM_PRIO=0 disables; AGFT_PRIO_ORDER="3,5,0,2,1,4"
+// overrides the order (class ids of agft_internal.cuh, highest priority first).
 cudaError_t create_streams(agft_handle h)
 {
     cudaError_t e = cudaEventCreateWithFlags(&h->fork, cudaEventDisableTiming);
